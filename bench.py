@@ -1,0 +1,549 @@
+#!/usr/bin/env python
+"""Benchmark: frames/s + Gsamples/s of slice-based ray casting on B200.
+
+Default workload = BASELINE.json config 3: a 512^3 float32 sphere-blob volume
+(seed 7, TF "hot") rendered to 1024^2 with cone scattering from a 256-slice
+attenuation buffer at 512^2, step 1/512. One step = one frame = K1
+(attenuation build, the light is rebuilt every frame) + K2 (ray march) +
+image assembly (NCCL all-gather when N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--build replicated|sharded]
+    python bench.py --impl reference ...   # the reference CPU path (oracle port), all host cores
+
+Prints ONE JSON line on rank 0. Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks; inputs (512 MiB volume,
+256 MiB buffer) are larger than L2, so no explicit flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/s + Gsamples/s, 512³ vol→1024² image, 256 light slices, 1–8 GPU"
+LIGHT = (0.3, -0.5, 0.8)
+EYE, TARGET = (0.5, 0.5, -1.6), (0.5, 0.5, 0.5)
+
+CONFIGS = {
+    1: dict(name="64^3 f32 sphere blobs -> 128^2, 32 slices @128^2, shell", dims=64, volume="blobs", seed=7,
+            tf="hot", n=32, res=128, image=128, step=1 / 256, mode="shell"),
+    2: dict(name="256^3 u8 perforated block -> 512^2, 128 slices @512^2, sbrc_shadow", dims=256, volume="block_u8",
+            seed=3, tf="bone", n=128, res=512, image=512, step=1 / 256, mode="sbrc_shadow"),
+    3: dict(name="512^3 f32 sphere blobs -> 1024^2, 256 slices @512^2, cone", dims=512, volume="blobs", seed=7,
+            tf="hot", n=256, res=512, image=1024, step=1 / 512, mode="cone"),
+    4: dict(name="1024^3 u16 sphere blobs -> 2048^2, 512 slices @1024^2, cone", dims=1024, volume="blobs_u16",
+            seed=7, tf="hot", n=512, res=1024, image=2048, step=1 / 1024, mode="cone"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default=None, help="override shading mode")
+    ap.add_argument("--build", choices=("replicated", "sharded"), default="replicated")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extra", action="store_true", help="also print a per-kernel detail line to stderr")
+    a = ap.parse_args()
+    a.warmup = max(a.warmup, 3)
+    return a
+
+
+# --------------------------------------------------------------- scene inputs
+def scene_objects(cfg, mode):
+    from paper_2008_06134_b200 import scene
+    tf = scene.preset(cfg["tf"])
+    cam = scene.LightCamera.fit(LIGHT, (1.0, 1.0, 1.0), (cfg["res"], cfg["res"]))
+    spec = scene.make_slice_stack(LIGHT, cfg["n"])
+    settings = scene.RenderSettings(camera=scene.Camera(position=EYE, target=TARGET), light=scene.Light(direction=LIGHT),
+                                    viewport=(cfg["image"], cfg["image"]), step=cfg["step"], shading_mode=mode)
+    return tf, cam, spec, settings
+
+
+def host_volume(cfg):
+    """The config's volume as a host VolumeDataset (numpy; bit-identical to the reference generators)."""
+    from paper_2008_06134_b200 import datasets
+    d = cfg["dims"]
+    if cfg["volume"] == "block_u8":
+        return datasets.raw_roundtrip(datasets.make_perforated_block((d, d, d), seed=cfg["seed"]), "u8")
+    field = np.empty((d, d, d), dtype=np.float32)
+    step = max(1, min(d, (1 << 24) // (d * d)))
+    for z0 in range(0, d, step):  # z-slabs bound host memory; per-voxel formula unchanged
+        field[z0:z0 + step] = _blob_slab(d, cfg["seed"], z0, min(d, z0 + step))
+    from paper_2008_06134_b200.scene import VolumeDataset
+    if cfg["volume"] == "blobs_u16":
+        return datasets.raw_roundtrip(VolumeDataset.from_array(field), "u16")
+    return VolumeDataset.from_array(field)
+
+
+def _blob_slab(d, seed, z0, z1):
+    from paper_2008_06134_b200.datasets import _blob_params
+    ax = (np.arange(d) + 0.5) / d
+    zs = (np.arange(z0, z1) + 0.5) / d
+    zz, yy, xx = np.meshgrid(zs, ax, ax, indexing="ij")
+    acc = np.zeros_like(xx)
+    for c, s, a in _blob_params(seed, 5):
+        acc += a * np.exp(-((xx - c[0]) ** 2 + (yy - c[1]) ** 2 + (zz - c[2]) ** 2) / (2.0 * s * s))
+    return np.clip(acc, 0.0, 1.0).astype(np.float32)
+
+
+def device_volume_for(cfg, dev):
+    """Generate the config's volume directly in HBM (float64 formula on the GPU)."""
+    import torch
+    from paper_2008_06134_b200 import datasets
+    from paper_2008_06134_b200.device import DeviceVolume
+    d = cfg["dims"]
+    if cfg["volume"] == "block_u8":
+        v = host_volume(cfg)
+        return DeviceVolume.from_dataset(v, dev), v
+    q = "u16" if cfg["volume"] == "blobs_u16" else None
+    t = datasets.sphere_blobs_device((d, d, d), seed=cfg["seed"], device=dev, quantize_to=q)
+    kind = 2 if q else 0
+    one = np.ones(3)
+    return DeviceVolume(t, kind, (d, d, d), np.zeros(3), one), None
+
+
+def algorithmic_bytes(cfg, voxel_bytes, world):
+    """K1 = V + A (sharded: V + A/G); K2 = V + A + I/G (buffer modes)."""
+    V = cfg["dims"] ** 3 * voxel_bytes
+    A = 4 * cfg["n"] * cfg["res"] ** 2
+    I = 16 * cfg["image"] ** 2
+    return V, A, I
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 50 ms; ``mark()``
+    brackets the timed region and only samples inside it are summarised."""
+
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def __enter__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.4)
+        return self
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        import datetime as _dt
+        if self.proc is None:
+            return None
+        self.f.flush()
+        self.f.seek(0)
+        rows = []
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.f.read().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                ts = _dt.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]), float(parts[3]),
+                             [nm for nm, val in zip(names, parts[4:8]) if val.lower() == "active"]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        inside = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
+        if not inside:  # timed region shorter than the sampling period: nearest sample after start
+            after = [r for r in rows if self.t0 is None or r[0] >= self.t0]
+            inside = after[:1] or rows[-1:]
+        reasons = sorted({nm for r in inside for nm in r[4]})
+        return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": inside[0][2],
+                "power_w_max": max(r[3] for r in inside), "reasons": reasons, "samples": len(inside),
+                "window_s": (self.t1 - self.t0) if (self.t0 and self.t1) else None}
+
+
+# --------------------------------------------------------------- CPU sample
+def cpu_sample_plan(cfg):
+    """Bounded, stratified sample of one frame for the CPU path: every 16th light
+    row for the build, rows/cols 6::12 of the image for the march."""
+    res, img = cfg["res"], cfg["image"]
+    b_rows = np.arange(8, res, 16) if res >= 32 else np.arange(res)
+    stride = 12 if img >= 256 else 1
+    p_rows = np.arange(6, img, stride) if stride > 1 else np.arange(img)
+    return b_rows, p_rows
+
+
+def _cpu_build_part(args):
+    rows, = args
+    from oracle import slicecast_oracle as O
+    g = _CPU_CTX
+    t = time.perf_counter()
+    O.build_intensity(g["vol"], g["tf"].lut, g["cam"], g["spec"], 0.0, rows=rows)
+    return time.perf_counter() - t
+
+
+def _cpu_march_part(args):
+    rows, cols = args
+    from oracle import slicecast_oracle as O
+    g = _CPU_CTX
+    t = time.perf_counter()
+    _, n = O.render_image(g["vol"], g["tf"].lut, g["settings"], g["buffer"], rows=rows, cols=cols,
+                          return_samples=True)
+    return time.perf_counter() - t, n
+
+
+_CPU_CTX: dict = {}
+
+
+def set_cpu_context(vol, tf, cam, spec, settings, intensity):
+    """State the CPU workers read (set before forking a pool)."""
+    from paper_2008_06134_b200.lightbuffer import AttenuationBuffer
+    _CPU_CTX.update(vol=vol, tf=tf, cam=cam, spec=spec, settings=settings,
+                    buffer=AttenuationBuffer(cam, spec, 0.0, intensity) if intensity is not None else None)
+
+
+def cpu_frame_sample(cfg, workers=1, pool=None):
+    """Time the oracle on the bounded sample of one frame; extrapolate to the
+    full frame. Returns (frame_seconds, detail)."""
+    b_rows, p_rows = cpu_sample_plan(cfg)
+    t0 = time.perf_counter()
+    if pool is None:
+        _cpu_build_part((b_rows,))
+    else:
+        list(pool.map(_cpu_build_part, [(c,) for c in np.array_split(b_rows, workers) if len(c)]))
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    if pool is None:
+        _, samples = _cpu_march_part((p_rows, p_rows))
+    else:
+        parts = list(pool.map(_cpu_march_part, [(r, p_rows) for r in np.array_split(p_rows, workers) if len(r)]))
+        samples = sum(n for _, n in parts)
+    t_march = time.perf_counter() - t0
+    full_build = t_build * cfg["res"] / len(b_rows)
+    full_march = t_march * cfg["image"] ** 2 / (len(p_rows) ** 2)
+    detail = dict(build_rows=int(len(b_rows)), march_pixels=int(len(p_rows) ** 2), march_samples=int(samples),
+                  t_build_s=t_build, t_march_s=t_march, build_s_extrapolated=full_build,
+                  march_s_extrapolated=full_march)
+    return full_build + full_march, detail
+
+
+def _cpu_full_build_part(args):
+    rows, = args
+    from oracle import slicecast_oracle as O
+    g = _CPU_CTX
+    return O.build_intensity(g["vol"], g["tf"].lut, g["cam"], g["spec"], 0.0, rows=rows)
+
+
+def cpu_sample_text(cfg):
+    b_rows, p_rows = cpu_sample_plan(cfg)
+    return (f"oracle (numpy port of the reference) on a stratified sample of one frame: build on "
+            f"{len(b_rows)}/{cfg['res']} light rows, march on {len(p_rows)}x{len(p_rows)} of "
+            f"{cfg['image']}x{cfg['image']} pixels; frame time extrapolated by row/pixel count")
+
+
+# --------------------------------------------------------------- reference arm
+def run_reference(a, cfg, mode):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    tf, cam, spec, settings = scene_objects(cfg, mode)
+    vol = host_volume(cfg)
+    workers = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    ctx = mp.get_context("fork")
+    inten = None
+    if mode != "none":  # the march reads the full stack: build it once, untimed, on all cores
+        set_cpu_context(vol, tf, cam, spec, settings, None)
+        with ctx.Pool(workers) as pool:
+            parts = pool.map(_cpu_full_build_part, [(c,) for c in np.array_split(np.arange(cfg["res"]), workers)
+                                                    if len(c)])
+        inten = np.concatenate(parts, axis=1)
+    set_cpu_context(vol, tf, cam, spec, settings, inten)
+    with ctx.Pool(workers) as pool:
+        for _ in range(a.warmup):
+            cpu_frame_sample(cfg, workers, pool)
+        times = []
+        detail = None
+        for _ in range(a.steps):
+            ft, detail = cpu_frame_sample(cfg, workers, pool)
+            times.append(ft)
+    frame_s = statistics.median(times)
+    fps = 1.0 / frame_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {a.config}: {cfg['name']}", "shading_mode": mode,
+                   "parallelism": f"cpu processes x{workers}", "l2": "n/a (CPU)"},
+        "gsamples_per_s": detail["march_samples"] / max(detail["t_march_s"], 1e-12) / 1e9,
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": "port",
+                         "sample": cpu_sample_text(cfg), "detail": detail},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(a, cfg, mode):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2008_06134_b200 as sb
+    from paper_2008_06134_b200.frame import FrameRenderer
+
+    tf, cam, spec, settings = scene_objects(cfg, mode)
+    t0 = time.perf_counter()
+    dvol, host_vol = device_volume_for(cfg, dev)
+    torch.cuda.synchronize()
+    vol_gen_s = time.perf_counter() - t0
+    fr = FrameRenderer(dvol, tf, cam, spec, settings, build=a.build if world > 1 else "replicated",
+                       band_rows=8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    # samples per frame (deterministic): one counted frame
+    fr.reset_counter()
+    fr.frame()
+    torch.cuda.synchronize()
+    samples = int(fr.counter.item())
+    if world > 1:
+        t = torch.tensor([samples], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        samples = int(t.item())
+
+    def one_step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        fr.build()
+        if ev is not None:
+            ev[1].record(stream)
+        fr.march(count_samples=False)
+        if ev is not None:
+            ev[2].record(stream)
+        fr.assemble()
+        if ev is not None:
+            ev[3].record(stream)
+
+    for _ in range(a.warmup):
+        one_step()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        clocks.mark("t0")
+        start.record(stream)
+        for i in range(a.steps):
+            one_step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+        clocks.mark("t1")
+    if world > 1:
+        dist.barrier()
+    total_ms = start.elapsed_time(end)
+    k1 = [e[0].elapsed_time(e[1]) for e in evs]
+    k2 = [e[1].elapsed_time(e[2]) for e in evs]
+    asm = [e[2].elapsed_time(e[3]) for e in evs]
+    stats = torch.tensor([total_ms, sum(k1) / len(k1), sum(k2) / len(k2), sum(asm) / len(asm)],
+                         dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    total_ms, k1_ms, k2_ms, asm_ms = stats.tolist()
+    ms_per_step = total_ms / a.steps
+    fps = 1000.0 / ms_per_step
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        e2e = e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev)
+
+    # ---- roofline of the dominant kernel
+    vbytes = dvol.data.element_size()
+    V, A, I = algorithmic_bytes(cfg, vbytes, world)
+    k1_bytes = V + (A if (world == 1 or a.build == "replicated") else A // world)
+    k2_bytes = (V + A + I // world) if mode != "none" else (V + I // world)
+    peaks = load_peaks()
+    dominant = "march" if k2_ms >= k1_ms else "build"
+    d_bytes, d_ms = (k2_bytes, k2_ms) if dominant == "march" else (k1_bytes, k1_ms)
+    achieved = d_bytes / (d_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["source"],
+                "algorithmic_bytes": d_bytes, "kernel_ms": d_ms,
+                "traffic": load_traffic(a.config, mode, dominant)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        inten = fr.intensity.contiguous().cpu().numpy() if mode != "none" else None
+        cpu = cpu_baseline_leg(cfg, tf, cam, spec, settings, dvol, host_vol, inten)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {a.config}: {cfg['name']}", "volume": f"{cfg['dims']}^3 "
+                       + ("f32" if vbytes == 4 else ("u16" if vbytes == 2 else "u8")),
+                       "image": [cfg["image"], cfg["image"]], "n_slices": cfg["n"],
+                       "slice_res": [cfg["res"], cfg["res"]], "step": cfg["step"], "shading_mode": mode,
+                       "build": a.build if world > 1 else "single", "parallelism": f"image-tiles x{world}",
+                       "l2": "inputs larger than L2 (volume %d MiB, buffer %d MiB)" % (V >> 20, A >> 20)},
+            "gsamples_per_s": samples / (k2_ms * 1e-3) / 1e9,
+            "samples_per_frame": samples,
+            "kernels": {"build_ms": k1_ms, "march_ms": k2_ms, "assemble_ms": asm_ms,
+                        "build_gbs": k1_bytes / (k1_ms * 1e-3) / 1e9, "march_gbs": k2_bytes / (k2_ms * 1e-3) / 1e9,
+                        "build_gtexel_slices_s": cfg["n"] * cfg["res"] ** 2 / (k1_ms * 1e-3) / 1e9},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 2 * a.steps,
+            "clocks": clocks.summary(),
+            "volume_gen_s": vol_gen_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
+    """Same frame through the public API with host buffers: LUTs and slice
+    offsets copied host->device every step, the image read back to host.
+    The volume is uploaded once (device cache keyed by the host array, as the
+    reference service keeps datasets resident) and that upload is reported
+    separately."""
+    import torch
+    import paper_2008_06134_b200 as sb
+    if host_vol is None:
+        from paper_2008_06134_b200.scene import VolumeDataset
+        raw = dvol.data.cpu().numpy()
+        if dvol.voxel_type == 0:
+            host_vol = VolumeDataset.from_array(raw)
+        else:
+            host_vol = VolumeDataset.from_raw_array(raw.view(np.uint16) if dvol.voxel_type == 2 else raw)
+    t0 = time.perf_counter()
+    if world == 1:
+        from paper_2008_06134_b200.device import device_volume
+        device_volume(host_vol, dev)
+        torch.cuda.synchronize()
+    upload_s = time.perf_counter() - t0
+    n = int(spec.n_slices)
+    h2d = 256 * 4 * 8 + 256 * 8 + n * 8
+    d2h = cfg["image"] ** 2 * 16
+
+    def step():
+        if world == 1:
+            buf = sb.build_attenuation_buffer(host_vol, tf, cam, spec)
+            img = sb.render(host_vol, tf, settings, buf)
+        else:
+            fr.lut.copy_(torch.from_numpy(tf.resolve(settings.step)))
+            fr.alpha.copy_(torch.from_numpy(np.ascontiguousarray(tf.resolve(spec.spacing)[:, 3])))
+            fr.offsets.copy_(torch.from_numpy(spec.plane_offsets))
+            img = fr.frame().cpu().numpy()
+        return img
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    k = max(3, a.steps // 2)
+    for _ in range(k):
+        step()
+    torch.cuda.synchronize()
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    sec = el.item() / k
+    return {"value": 1.0 / sec, "unit": "frames/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": sec * 1e3, "steps": k, "volume_upload_s_once": upload_s,
+            "path": "paper_2008_06134_b200.build_attenuation_buffer + render (numpy in, numpy out)"
+            if world == 1 else "FrameRenderer (host LUTs in, host image out)"}
+
+
+def cpu_baseline_leg(cfg, tf, cam, spec, settings, dvol, host_vol, intensity):
+    """The oracle port, single thread, on the bounded sample of this workload.
+    The march reads the GPU-built stack (bit-identical to the oracle's, see tests)."""
+    from paper_2008_06134_b200.scene import VolumeDataset
+    if host_vol is None:
+        raw = dvol.data.cpu().numpy()
+        host_vol = VolumeDataset.from_array(raw) if dvol.voxel_type == 0 else \
+            VolumeDataset.from_raw_array(raw.view(np.uint16) if dvol.voxel_type == 2 else raw)
+    set_cpu_context(host_vol, tf, cam, spec, settings, intensity)
+    frame_s, detail = cpu_frame_sample(cfg)
+    return {"value": 1.0 / frame_s, "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": cpu_sample_text(cfg), "detail": detail}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_traffic(config, mode, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"config{config}/{mode}/{kernel}")
+    except (OSError, ValueError):
+        return None
+
+
+def main():
+    a = parse()
+    cfg = CONFIGS[a.config]
+    mode = a.mode or cfg["mode"]
+    if a.impl == "reference":
+        return run_reference(a, cfg, mode)
+    return run_ours(a, cfg, mode)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,169 @@
+/*
+ * sbrc.h — C ABI of the B200 slice-based ray-casting hot path.
+ *
+ * Two entry points replace the two numpy functions of the reference
+ * package `slicecast` (arXiv 2008.06134, /root/reference/pkg/src/slicecast):
+ *
+ *   sbrc_build   <- build_attenuation_buffer(v, tf, cam, spec, compensation_n)
+ *                   lightbuffer.py:144-199 (Alg. 1)
+ *   sbrc_render  <- render(v, tf, settings, buffer) -> (H, W, 4) float32
+ *                   raycaster.py:443-469, with _march_rays :415-440,
+ *                   _make_shader :376-412, lookup_light_scalar_many
+ *                   lightbuffer.py:256-287, _shell_scalar :239-250,
+ *                   _cone_scalar :266-300.
+ *
+ * Conventions
+ *  - Every pointer inside a params struct is a DEVICE pointer; the structs
+ *    themselves live in host memory and are copied into the kernel launch.
+ *  - The library allocates nothing persistent, keeps no global mutable
+ *    state, never synchronises, and enqueues on `stream` (a cudaStream_t,
+ *    NULL = legacy default stream). Calls on distinct streams are safe to
+ *    issue concurrently (the reference functions are reentrant, raycaster.py:447).
+ *  - Return value: SBRC_OK (0) or a negative sbrc_status. Parameters are
+ *    validated before launch; launch errors are reported as SBRC_ECUDA.
+ *    The Python shim maps EINVAL -> ValueError, ECONFIG -> ConfigError,
+ *    ECUDA -> RuntimeError (the reference's exception types).
+ *  - Setup quantities are float64 exactly as the reference computes them
+ *    (numpy float64); decisions (cube coverage, ray entry/exit, sample
+ *    count, early termination) are evaluated in float64 with the numpy
+ *    operation order and no FMA contraction, so they match bit for bit.
+ */
+#ifndef SBRC_H
+#define SBRC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBRC_ABI_VERSION 1
+#define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
+#define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
+#define SBRC_LUT_SIZE 256   /* transfer.py:16 */
+
+typedef enum sbrc_status {
+  SBRC_OK = 0,
+  SBRC_EINVAL = -1,      /* bad parameter (ValueError in the reference)        */
+  SBRC_ECONFIG = -2,     /* buffer mode without a buffer (ConfigError, raycaster.py:450) */
+  SBRC_ECUDA = -3,       /* CUDA launch / runtime error                        */
+  SBRC_EUNSUPPORTED = -4 /* mode the hot path does not implement (phong, extinction) */
+} sbrc_status;
+
+typedef enum sbrc_voxel_type {
+  SBRC_VOXEL_F32 = 0, /* already-normalised float32 (volume.py:147-149)          */
+  SBRC_VOXEL_U8 = 1,  /* raw u8, normalised at fetch as (float)x / 255.0f (volume.py:143-144) */
+  SBRC_VOXEL_U16 = 2  /* raw u16, normalised at fetch as (float)x / 65535.0f (volume.py:145-146) */
+} sbrc_voxel_type;
+
+typedef enum sbrc_shading {
+  SBRC_SHADE_NONE = 0,   /* "none"        raycaster.py:383-384 */
+  SBRC_SHADE_SHADOW = 1, /* "sbrc_shadow" raycaster.py:398-401 */
+  SBRC_SHADE_SHELL = 2,  /* "shell"       raycaster.py:402-406 */
+  SBRC_SHADE_CONE = 3    /* "cone"        raycaster.py:407-411 */
+} sbrc_shading;
+
+typedef enum sbrc_lookup {
+  SBRC_LOOKUP_LINEAR = 0, /* lightbuffer.py:277-285 */
+  SBRC_LOOKUP_NEAREST = 1 /* lightbuffer.py:274-276 */
+} sbrc_lookup;
+
+/* VolumeDataset (volume.py:61-122): voxel (x,y,z) at x + nx*(y + ny*z). */
+typedef struct sbrc_volume {
+  const void* data;   /* device, nx*ny*nz voxels of voxel_type        */
+  int32_t nx, ny, nz;
+  int32_t voxel_type; /* sbrc_voxel_type                               */
+  double box_lo[3];   /* VolumeDataset.box_lo                          */
+  double box_ext[3];  /* box_hi - box_lo, as numpy computes it         */
+} sbrc_volume;
+
+/* LightCamera (lightbuffer.py:37-86) + SliceStackSpec (slicing.py:22-33). */
+typedef struct sbrc_light_frame {
+  int32_t width, height;  /* LightCamera.resolution (W, H)             */
+  int32_t n_slices;       /* SliceStackSpec.n_slices                    */
+  int32_t _pad;
+  double axis_u[3], axis_v[3];
+  double light_dir[3];    /* SliceStackSpec.light_dir (normalised)      */
+  double u_range[2], v_range[2];
+  double d_min, d_max;
+  const double* plane_offsets; /* device, n_slices float64 (build only) */
+} sbrc_light_frame;
+
+typedef struct sbrc_build_params {
+  sbrc_volume volume;
+  sbrc_light_frame light;
+  const double* alpha_lut; /* device, 256 float64 = tf.resolve(spec.spacing)[:, 3] */
+  double compensation_n;   /* lightbuffer.py:193-196                    */
+  int32_t row_begin;       /* light-plane rows [row_begin, row_end) are built; */
+  int32_t row_end;         /* full build: 0, height (row-sharded build otherwise) */
+  /* output: intensity(k, y, x) stored at out[k*layer_stride + (y-row_begin)*row_stride + x];
+   * the reference (n, H, W) layout is layer_stride = H*W, row_stride = W; the
+   * row-major [H][n][W] layout (a row shard is contiguous) is layer_stride = W,
+   * row_stride = n*W. */
+  int64_t layer_stride;
+  int64_t row_stride;
+  float* out;
+} sbrc_build_params;
+
+typedef struct sbrc_render_params {
+  sbrc_volume volume;
+  const double* lut_rgba;  /* device, 256x4 float64 = tf.resolve(settings.step) */
+  int32_t width, height;   /* RenderSettings.viewport (W, H)            */
+  int32_t shading;         /* sbrc_shading                              */
+  int32_t lookup;          /* sbrc_lookup                               */
+  /* Camera.rays (raycaster.py:53-68): host computes the basis with numpy */
+  double eye[3], forward[3], right[3], up2[3];
+  double tan_half, aspect;
+  double step;             /* RenderSettings.step                       */
+  double et_alpha;         /* RenderSettings.early_termination_alpha    */
+  /* attenuation buffer (buffer modes only) */
+  sbrc_light_frame light;
+  const float* intensity;  /* device float32; texel (k, y, x) at
+                              intensity[k*layer_stride + y*row_stride + x] */
+  int64_t layer_stride, row_stride;
+  float light_color[3];
+  float ambient_floor;
+  /* ShellKernel: radii/weights (raycaster.py:91-109) */
+  int32_t shell_count;
+  int32_t cone_axis_samples;      /* ConeKernel.axis_samples              */
+  int32_t cone_angle_count;
+  int32_t _pad;
+  double shell_radius[SBRC_MAX_SHELLS];
+  double shell_weight[SBRC_MAX_SHELLS];
+  double cone_ring;                /* ConeKernel.ring_radius_per_step     */
+  double cone_cos[SBRC_MAX_ANGLES], cone_sin[SBRC_MAX_ANGLES];
+  /* image-space partition: rows grouped in bands of band_rows; band b is
+   * rendered by rank b % world into rank-local row (b / world)*band_rows + r */
+  int32_t band_rows, rank, world, _pad2;
+  float* image;                    /* device, rank-local (rows, W, 4) premultiplied rgba */
+  unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
+} sbrc_render_params;
+
+/* ABI version of the loaded library (== SBRC_ABI_VERSION). */
+int sbrc_abi_version(void);
+
+/* Human-readable text for a status code (static storage). */
+const char* sbrc_strerror(int status);
+
+/* sizeof() of the params structs, so a binding can verify its layout. */
+int64_t sbrc_struct_size(int which); /* 0 volume, 1 light_frame, 2 build, 3 render */
+
+/* K0: repack a raw voxel stream already on the device (no-op copy for f32;
+ * u8/u16 stay raw and are normalised at fetch). Replaces load_raw's
+ * normalisation (volume.py:141-151) for the device copy. */
+int sbrc_volume_check(const sbrc_volume* v);
+
+/* K1: attenuation build (lightbuffer.py:144-199). */
+int sbrc_build(const sbrc_build_params* p, void* stream);
+
+/* K2: ray march (raycaster.py:443-469). Writes the rank-local rows. */
+int sbrc_render(const sbrc_render_params* p, void* stream);
+
+/* Number of rank-local image rows sbrc_render writes for (height, band_rows, rank, world). */
+int sbrc_local_rows(int height, int band_rows, int rank, int world);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SBRC_H */

@@ -1,0 +1,112 @@
+"""ctypes binding of the sbrc C ABI (include/sbrc.h).
+
+The shared library ``_sbrc.so`` is built in-tree by ``build.py`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``). There is no fallback: if the
+library is missing this module raises ImportError at import time, and every
+call checks the returned status.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .scene import ConfigError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_sbrc.so")
+
+ABI_VERSION = 1
+MAX_SHELLS = 8
+MAX_ANGLES = 16
+
+OK, EINVAL, ECONFIG, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4
+VOXEL_F32, VOXEL_U8, VOXEL_U16 = 0, 1, 2
+SHADE = {"none": 0, "sbrc_shadow": 1, "shell": 2, "cone": 3}
+LOOKUP = {"linear": 0, "nearest": 1}
+
+#: every symbol include/sbrc.h declares
+EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume_check",
+           "sbrc_build", "sbrc_render", "sbrc_local_rows")
+
+D3 = C.c_double * 3
+D2 = C.c_double * 2
+
+
+class SbrcVolume(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+                ("voxel_type", C.c_int32), ("box_lo", D3), ("box_ext", D3)]
+
+
+class SbrcLightFrame(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("n_slices", C.c_int32),
+                ("_pad", C.c_int32), ("axis_u", D3), ("axis_v", D3), ("light_dir", D3),
+                ("u_range", D2), ("v_range", D2), ("d_min", C.c_double), ("d_max", C.c_double),
+                ("plane_offsets", C.c_void_p)]
+
+
+class SbrcBuildParams(C.Structure):
+    _fields_ = [("volume", SbrcVolume), ("light", SbrcLightFrame), ("alpha_lut", C.c_void_p),
+                ("compensation_n", C.c_double), ("row_begin", C.c_int32), ("row_end", C.c_int32),
+                ("layer_stride", C.c_int64), ("row_stride", C.c_int64), ("out", C.c_void_p)]
+
+
+class SbrcRenderParams(C.Structure):
+    _fields_ = [("volume", SbrcVolume), ("lut_rgba", C.c_void_p),
+                ("width", C.c_int32), ("height", C.c_int32), ("shading", C.c_int32), ("lookup", C.c_int32),
+                ("eye", D3), ("forward", D3), ("right", D3), ("up2", D3),
+                ("tan_half", C.c_double), ("aspect", C.c_double), ("step", C.c_double),
+                ("et_alpha", C.c_double), ("light", SbrcLightFrame), ("intensity", C.c_void_p),
+                ("layer_stride", C.c_int64), ("row_stride", C.c_int64),
+                ("light_color", C.c_float * 3), ("ambient_floor", C.c_float),
+                ("shell_count", C.c_int32), ("cone_axis_samples", C.c_int32),
+                ("cone_angle_count", C.c_int32), ("_pad", C.c_int32),
+                ("shell_radius", C.c_double * MAX_SHELLS), ("shell_weight", C.c_double * MAX_SHELLS),
+                ("cone_ring", C.c_double), ("cone_cos", C.c_double * MAX_ANGLES),
+                ("cone_sin", C.c_double * MAX_ANGLES),
+                ("band_rows", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("_pad2", C.c_int32),
+                ("image", C.c_void_p), ("sample_count", C.c_void_p)]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"sbrc CUDA library not built: {LIB_PATH} is missing "
+            "(run `python paper_2008_06134_b200/build.py` or __graft_entry__.build())")
+    lib = C.CDLL(LIB_PATH)
+    lib.sbrc_abi_version.restype = C.c_int
+    lib.sbrc_strerror.restype = C.c_char_p
+    lib.sbrc_strerror.argtypes = [C.c_int]
+    lib.sbrc_struct_size.restype = C.c_int64
+    lib.sbrc_struct_size.argtypes = [C.c_int]
+    lib.sbrc_volume_check.argtypes = [C.POINTER(SbrcVolume)]
+    lib.sbrc_build.argtypes = [C.POINTER(SbrcBuildParams), C.c_void_p]
+    lib.sbrc_render.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p]
+    lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    if lib.sbrc_abi_version() != ABI_VERSION:
+        raise ImportError(f"sbrc ABI mismatch: library {lib.sbrc_abi_version()} != binding {ABI_VERSION}")
+    sizes = (SbrcVolume, SbrcLightFrame, SbrcBuildParams, SbrcRenderParams)
+    for i, st in enumerate(sizes):
+        if lib.sbrc_struct_size(i) != C.sizeof(st):
+            raise ImportError(f"sbrc struct {st.__name__} layout mismatch: "
+                              f"C {lib.sbrc_struct_size(i)} vs ctypes {C.sizeof(st)}")
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int, what: str) -> None:
+    """Map a C status to the reference's exception types."""
+    if status == OK:
+        return
+    msg = f"{what}: {lib.sbrc_strerror(status).decode()}"
+    if status == ECONFIG:
+        raise ConfigError(msg)
+    if status in (EINVAL, EUNSUPPORTED):
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def local_rows(height: int, band_rows: int, rank: int, world: int) -> int:
+    return int(lib.sbrc_local_rows(height, band_rows, rank, world))

@@ -1,0 +1,201 @@
+"""Device residency: volume upload (K0), LUT upload and C-ABI parameter packing.
+
+Volume (K0). The reference keeps a float32 (nz, ny, nx) array normalised at
+load time (volume.py:141-151). On the device we keep the *raw* voxels when
+the dataset came from u8/u16 (1 or 2 bytes per voxel instead of 4): the
+kernels renormalise at fetch with an IEEE float32 division, which gives the
+same float32 value bit for bit. A volume is uploaded once and cached by
+array identity, the way the reference service keeps datasets resident
+(service.py:133-152); later calls with the same array only re-use it.
+"""
+
+from __future__ import annotations
+
+import math
+import weakref
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .scene import camera_frame, ShellKernel, ConeKernel
+
+
+def _require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2008_06134_b200 needs a CUDA device (sm_100a); there is no CPU path")
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def current_stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class DeviceVolume:
+    """A VolumeDataset resident in HBM in its compact stored encoding."""
+
+    def __init__(self, data: torch.Tensor, voxel_type: int, dims, box_lo, box_hi):
+        self.data = data
+        self.voxel_type = voxel_type
+        self.dims = tuple(int(d) for d in dims)
+        self.box_lo = np.asarray(box_lo, dtype=np.float64)
+        self.box_hi = np.asarray(box_hi, dtype=np.float64)
+
+    @property
+    def voxel_size(self) -> np.ndarray:
+        """(box_hi - box_lo) / dims, as VolumeDataset.voxel_size (volume.py:119-122)."""
+        return (self.box_hi - self.box_lo) / np.array(self.dims, dtype=np.float64)
+
+    @property
+    def nbytes(self) -> int:
+        return self.data.numel() * self.data.element_size()
+
+    def struct(self) -> N.SbrcVolume:
+        s = N.SbrcVolume()
+        s.data = self.data.data_ptr()
+        s.nx, s.ny, s.nz = self.dims
+        s.voxel_type = self.voxel_type
+        s.box_lo[:] = [float(x) for x in self.box_lo]
+        s.box_ext[:] = [float(x) for x in (self.box_hi - self.box_lo)]
+        return s
+
+    @classmethod
+    def from_dataset(cls, v, device=None, raw: np.ndarray | None = None) -> "DeviceVolume":
+        """Upload ``v`` (a VolumeDataset, ours or the reference's).
+
+        ``raw`` optionally supplies the u8/u16 voxels; otherwise, for a u8/u16
+        dataset, they are recovered from ``v.data`` and kept only if they
+        reproduce ``v.data`` exactly."""
+        dev = _require_cuda(device)
+        data = np.ascontiguousarray(v.data, dtype=np.float32)
+        kind, stored = N.VOXEL_F32, data
+        scalar_type = getattr(v, "scalar_type", "f32")
+        if raw is None and scalar_type in ("u8", "u16"):
+            scale, dt = (255.0, np.uint8) if scalar_type == "u8" else (65535.0, np.uint16)
+            cand = np.rint(data.astype(np.float64) * scale)
+            if cand.min() >= 0 and cand.max() <= scale:
+                cand = cand.astype(dt)
+                if np.array_equal(cand.astype(np.float32) / np.float32(scale), data):
+                    raw = cand
+        if raw is not None:
+            raw = np.ascontiguousarray(raw)
+            kind = {np.dtype(np.uint8): N.VOXEL_U8, np.dtype(np.uint16): N.VOXEL_U16}[raw.dtype]
+            stored = raw.view(np.int16) if raw.dtype == np.uint16 else raw
+        t = torch.from_numpy(stored).to(dev)
+        return cls(t, kind, v.dims, v.box_lo, v.box_hi)
+
+
+_VOLUME_CACHE: dict[int, tuple[weakref.ref, DeviceVolume]] = {}
+
+
+def device_volume(v, device=None) -> DeviceVolume:
+    """Cached upload keyed by the identity of ``v.data``."""
+    if isinstance(v, DeviceVolume):
+        return v
+    dv = getattr(v, "_device_volume", None)
+    if isinstance(dv, DeviceVolume):
+        return dv
+    key = id(v.data)
+    hit = _VOLUME_CACHE.get(key)
+    if hit is not None and hit[0]() is v.data and hit[1].data.device == _require_cuda(device):
+        return hit[1]
+    dvol = DeviceVolume.from_dataset(v, device)
+    try:
+        ref = weakref.ref(v.data, lambda _r, k=key: _VOLUME_CACHE.pop(k, None))
+        _VOLUME_CACHE[key] = (ref, dvol)
+    except TypeError:
+        pass
+    return dvol
+
+
+def f64_tensor(arr, device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
+
+
+def light_frame(cam, spec, offsets_dev: torch.Tensor | None) -> N.SbrcLightFrame:
+    """Pack LightCamera + SliceStackSpec (lightbuffer.py:37-86, slicing.py:22-33)."""
+    lf = N.SbrcLightFrame()
+    lf.width, lf.height = int(cam.resolution[0]), int(cam.resolution[1])
+    lf.n_slices = int(spec.n_slices)
+    lf.axis_u[:] = [float(x) for x in cam.axis_u]
+    lf.axis_v[:] = [float(x) for x in cam.axis_v]
+    lf.light_dir[:] = [float(x) for x in spec.light_dir]
+    lf.u_range[:] = [float(cam.u_range[0]), float(cam.u_range[1])]
+    lf.v_range[:] = [float(cam.v_range[0]), float(cam.v_range[1])]
+    lf.d_min, lf.d_max = float(spec.d_min), float(spec.d_max)
+    lf.plane_offsets = offsets_dev.data_ptr() if offsets_dev is not None else None
+    return lf
+
+
+def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, out: torch.Tensor,
+                 compensation_n: float, row_begin: int, row_end: int) -> N.SbrcBuildParams:
+    """``out`` is an (n, row_end-row_begin, W) float32 CUDA view with unit x stride."""
+    if out.dtype != torch.float32 or out.dim() != 3 or out.stride(2) != 1:
+        raise ValueError("build output must be an (n, rows, W) float32 view with contiguous rows")
+    p = N.SbrcBuildParams()
+    p.volume = dvol.struct()
+    p.light = light_frame(cam, spec, offsets_dev)
+    p.alpha_lut = alpha_lut_dev.data_ptr()
+    p.compensation_n = float(compensation_n)
+    p.row_begin, p.row_end = int(row_begin), int(row_end)
+    p.layer_stride, p.row_stride = int(out.stride(0)), int(out.stride(1))
+    p.out = out.data_ptr()
+    return p
+
+
+def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_cam, buffer_spec,
+                  intensity_dev: torch.Tensor | None, light_color, voxel_size_max: float,
+                  image: torch.Tensor, counter: torch.Tensor | None,
+                  band_rows: int = 8, rank: int = 0, world: int = 1) -> N.SbrcRenderParams:
+    """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469)."""
+    mode = settings.shading_mode
+    if mode not in N.SHADE:
+        raise ValueError(f"shading mode {mode!r} is not part of the GPU hot path "
+                         "(supported: none, sbrc_shadow, shell, cone)")
+    if settings.lookup_mode not in N.LOOKUP:
+        raise ValueError(f"unknown lookup mode {settings.lookup_mode!r}")
+    p = N.SbrcRenderParams()
+    p.volume = dvol.struct()
+    p.lut_rgba = lut_dev.data_ptr()
+    w, h = int(settings.viewport[0]), int(settings.viewport[1])
+    p.width, p.height = w, h
+    p.shading = N.SHADE[mode]
+    p.lookup = N.LOOKUP[settings.lookup_mode]
+    cam = settings.camera
+    fr = camera_frame(cam, settings.viewport)
+    p.eye[:] = [float(x) for x in cam.position]
+    p.forward[:] = [float(x) for x in fr["forward"]]
+    p.right[:] = [float(x) for x in fr["right"]]
+    p.up2[:] = [float(x) for x in fr["up2"]]
+    p.tan_half, p.aspect = fr["tan_half"], fr["aspect"]
+    p.step = float(settings.step)
+    p.et_alpha = float(settings.early_termination_alpha)
+    if mode != "none":
+        p.light = light_frame(buffer_cam, buffer_spec, None)
+        if intensity_dev is not None:
+            if intensity_dev.dtype != torch.float32 or intensity_dev.stride(2) != 1:
+                raise ValueError("intensity must be float32 with contiguous rows")
+            p.intensity = intensity_dev.data_ptr()
+            p.layer_stride, p.row_stride = int(intensity_dev.stride(0)), int(intensity_dev.stride(1))
+        p.light_color[:] = [float(c) for c in np.asarray(light_color, dtype=np.float64)]
+        p.ambient_floor = float(settings.ambient_floor)
+    if mode == "shell":
+        k = settings.shell_kernel or ShellKernel.default(float(voxel_size_max))
+        if len(k.radii) > N.MAX_SHELLS or len(k.radii) != len(k.weights) or not k.radii:
+            raise ValueError(f"shell kernel must have 1..{N.MAX_SHELLS} radii with matching weights")
+        p.shell_count = len(k.radii)
+        for i, (r, wt) in enumerate(zip(k.radii, k.weights)):
+            p.shell_radius[i], p.shell_weight[i] = float(r), float(wt)
+    if mode == "cone":
+        k = settings.cone_kernel or ConeKernel()
+        if not 1 <= len(k.angles) <= N.MAX_ANGLES:
+            raise ValueError(f"cone kernel must have 1..{N.MAX_ANGLES} angles")
+        p.cone_axis_samples = int(k.axis_samples)
+        p.cone_angle_count = len(k.angles)
+        p.cone_ring = float(k.ring_radius_per_step)
+        for i, th in enumerate(k.angles):
+            p.cone_cos[i], p.cone_sin[i] = math.cos(th), math.sin(th)
+    p.band_rows, p.rank, p.world = int(band_rows), int(rank), int(world)
+    p.image = image.data_ptr()
+    p.sample_count = counter.data_ptr() if counter is not None else None
+    return p

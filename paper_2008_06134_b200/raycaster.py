@@ -1,0 +1,72 @@
+"""Drop-in ``render`` on the GPU (K2).
+
+Mirrors ``slicecast.raycaster.render`` (raycaster.py:443-469): same
+arguments, the same ``ConfigError`` when a buffer mode has no buffer
+(:450-451), the same ``ValueError`` for an unknown lookup mode
+(lightbuffer.py:262-263), and a premultiplied RGBA float32 (H, W, 4) image
+with a transparent-black background. ``render`` returns numpy like the
+reference; ``render_device`` returns the CUDA tensor and optionally the
+executed-sample count.
+
+Modes on the hot path: ``none``, ``sbrc_shadow``, ``shell``, ``cone``.
+``phong`` and ``extinction`` are not part of it and raise.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import _require_cuda, current_stream_handle, device_volume, f64_tensor, render_params
+from .lightbuffer import AttenuationBuffer
+from .scene import BUFFER_MODES, ConfigError
+
+
+def _intensity_of(buffer, dev) -> torch.Tensor:
+    if isinstance(buffer, AttenuationBuffer):
+        return buffer.device_intensity(dev)
+    # a reference AttenuationBuffer (numpy intensity)
+    return torch.from_numpy(np.ascontiguousarray(buffer.intensity, dtype=np.float32)).to(dev)
+
+
+def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: bool = False,
+                  rank: int = 0, world: int = 1, band_rows: int = 8, out: torch.Tensor | None = None):
+    """Enqueue K2; returns the (rows, W, 4) CUDA image (all rows when world == 1)
+    and, with ``count_samples``, a 1-element int64 CUDA tensor of executed samples."""
+    mode = settings.shading_mode
+    if mode in BUFFER_MODES and buffer is None:
+        raise ConfigError(f"shading mode {mode!r} needs an attenuation buffer")
+    if settings.lookup_mode not in N.LOOKUP:
+        raise ValueError(f"unknown lookup mode {settings.lookup_mode!r}")
+    dev = _require_cuda(device)
+    dvol = device_volume(v, dev)
+    lut = f64_tensor(tf.resolve(settings.step), dev)   # raycaster.py:453
+    w, h = int(settings.viewport[0]), int(settings.viewport[1])
+    if world == 1:
+        band_rows = 8
+    rows = N.local_rows(h, band_rows, rank, world)  # padded to whole bands
+    if out is None:
+        out = torch.empty((max(rows, 1), w, 4), dtype=torch.float32, device=dev)
+    elif out.shape[0] < rows or out.shape[1] != w or out.shape[2] != 4 or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous ({rows}, {w}, 4) float32 tensor")
+    counter = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
+    inten, cam, spec, color = None, None, None, None
+    if mode in BUFFER_MODES:
+        inten = _intensity_of(buffer, dev)
+        cam, spec, color = buffer.camera, buffer.spec, buffer.camera.light_color
+        n, hh, ww = inten.shape
+        if (n, hh, ww) != (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0])):
+            raise ValueError("attenuation intensity shape does not match its camera/stack")
+    vs = float(dvol.voxel_size.max())   # ShellKernel.default(v.voxel_size.max()), :403
+    p = render_params(dvol, lut, settings, cam, spec, inten, color, vs, out, counter,
+                      band_rows=band_rows, rank=rank, world=world)
+    N.check(N.lib.sbrc_render(p, current_stream_handle()), "sbrc_render")
+    img = out[:h] if world == 1 else out
+    return (img, counter) if count_samples else img
+
+
+def render(v, tf, settings, buffer=None) -> np.ndarray:
+    """GPU ray cast; drop-in for raycaster.py:443-469 (returns numpy float32 (H, W, 4))."""
+    img = render_device(v, tf, settings, buffer)
+    return img.cpu().numpy()
