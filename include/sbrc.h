@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 1
+#define SBRC_ABI_VERSION 2
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -89,6 +89,14 @@ typedef struct sbrc_light_frame {
   const double* plane_offsets; /* device, n_slices float64 (build only) */
 } sbrc_light_frame;
 
+/* Texel quads. The attenuation stack I (n, H, W) (AttenuationBuffer.intensity,
+ * lightbuffer.py:114-115) is stored lookup-ready: the float4 at (k, y, x) is
+ *   ( I[k][y][x], I[k+][y][x], I[k][y][x+], I[k+][y][x+] ),
+ *   k+ = min(k+1, n-1), x+ = min(x+1, W-1),
+ * so the two-layer bilinear lookup of lookup_light_scalar_many
+ * (lightbuffer.py:238-287) is two 16-byte loads (rows y and y+1) instead of
+ * eight scalar gathers. I(k, y, x) is component 0 of quad (k, y, x). */
+
 typedef struct sbrc_build_params {
   sbrc_volume volume;
   sbrc_light_frame light;
@@ -96,13 +104,11 @@ typedef struct sbrc_build_params {
   double compensation_n;   /* lightbuffer.py:193-196                    */
   int32_t row_begin;       /* light-plane rows [row_begin, row_end) are built; */
   int32_t row_end;         /* full build: 0, height (row-sharded build otherwise) */
-  /* output: intensity(k, y, x) stored at out[k*layer_stride + (y-row_begin)*row_stride + x];
-   * the reference (n, H, W) layout is layer_stride = H*W, row_stride = W; the
-   * row-major [H][n][W] layout (a row shard is contiguous) is layer_stride = W,
-   * row_stride = n*W. */
-  int64_t layer_stride;
-  int64_t row_stride;
-  float* out;
+  /* output: texel quads (format above) of rows [row_begin, row_end);
+   * quad (k, y, x) at quads[4*((y-row_begin)*quad_row_stride + k*quad_layer_stride + x)] */
+  float* quads;
+  int64_t quad_layer_stride;  /* in float4 units; (n, H, W) layout: H*W, [H][n][W]: W   */
+  int64_t quad_row_stride;    /* in float4 units; (n, H, W) layout: W,   [H][n][W]: n*W */
 } sbrc_build_params;
 
 typedef struct sbrc_render_params {
@@ -118,9 +124,8 @@ typedef struct sbrc_render_params {
   double et_alpha;         /* RenderSettings.early_termination_alpha    */
   /* attenuation buffer (buffer modes only) */
   sbrc_light_frame light;
-  const float* intensity;  /* device float32; texel (k, y, x) at
-                              intensity[k*layer_stride + y*row_stride + x] */
-  int64_t layer_stride, row_stride;
+  const float* quads;      /* device texel quads of the attenuation stack */
+  int64_t quad_layer_stride, quad_row_stride;  /* float4 units */
   float light_color[3];
   float ambient_floor;
   /* ShellKernel: radii/weights (raycaster.py:91-109) */
@@ -158,6 +163,12 @@ int sbrc_build(const sbrc_build_params* p, void* stream);
 
 /* K2: ray march (raycaster.py:443-469). Writes the rank-local rows. */
 int sbrc_render(const sbrc_render_params* p, void* stream);
+
+/* Repack a plain float32 stack I(k, y, x) = plain[k*plain_layer_stride + y*plain_row_stride + x]
+ * (e.g. a host-built reference AttenuationBuffer.intensity uploaded as is) into texel quads. */
+int sbrc_pack_quads(const float* plain, int64_t plain_layer_stride, int64_t plain_row_stride,
+                    int n, int height, int width, float* quads, int64_t quad_layer_stride,
+                    int64_t quad_row_stride, void* stream);
 
 /* Number of rank-local image rows sbrc_render writes for (height, band_rows, rank, world). */
 int sbrc_local_rows(int height, int band_rows, int rank, int world);

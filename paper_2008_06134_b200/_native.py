@@ -16,7 +16,7 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_sbrc.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 
@@ -27,7 +27,7 @@ LOOKUP = {"linear": 0, "nearest": 1}
 
 #: every symbol include/sbrc.h declares
 EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume_check",
-           "sbrc_build", "sbrc_render", "sbrc_local_rows")
+           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_local_rows")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -48,7 +48,7 @@ class SbrcLightFrame(C.Structure):
 class SbrcBuildParams(C.Structure):
     _fields_ = [("volume", SbrcVolume), ("light", SbrcLightFrame), ("alpha_lut", C.c_void_p),
                 ("compensation_n", C.c_double), ("row_begin", C.c_int32), ("row_end", C.c_int32),
-                ("layer_stride", C.c_int64), ("row_stride", C.c_int64), ("out", C.c_void_p)]
+                ("quads", C.c_void_p), ("quad_layer_stride", C.c_int64), ("quad_row_stride", C.c_int64)]
 
 
 class SbrcRenderParams(C.Structure):
@@ -56,8 +56,8 @@ class SbrcRenderParams(C.Structure):
                 ("width", C.c_int32), ("height", C.c_int32), ("shading", C.c_int32), ("lookup", C.c_int32),
                 ("eye", D3), ("forward", D3), ("right", D3), ("up2", D3),
                 ("tan_half", C.c_double), ("aspect", C.c_double), ("step", C.c_double),
-                ("et_alpha", C.c_double), ("light", SbrcLightFrame), ("intensity", C.c_void_p),
-                ("layer_stride", C.c_int64), ("row_stride", C.c_int64),
+                ("et_alpha", C.c_double), ("light", SbrcLightFrame), ("quads", C.c_void_p),
+                ("quad_layer_stride", C.c_int64), ("quad_row_stride", C.c_int64),
                 ("light_color", C.c_float * 3), ("ambient_floor", C.c_float),
                 ("shell_count", C.c_int32), ("cone_axis_samples", C.c_int32),
                 ("cone_angle_count", C.c_int32), ("_pad", C.c_int32),
@@ -83,6 +83,8 @@ def _load() -> C.CDLL:
     lib.sbrc_build.argtypes = [C.POINTER(SbrcBuildParams), C.c_void_p]
     lib.sbrc_render.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p]
     lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    lib.sbrc_pack_quads.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                    C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
     if lib.sbrc_abi_version() != ABI_VERSION:
         raise ImportError(f"sbrc ABI mismatch: library {lib.sbrc_abi_version()} != binding {ABI_VERSION}")
     sizes = (SbrcVolume, SbrcLightFrame, SbrcBuildParams, SbrcRenderParams)

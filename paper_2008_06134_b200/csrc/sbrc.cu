@@ -7,16 +7,25 @@
 //                       (raycaster.py:376-469) with lookup_light_scalar_many
 //                       (lightbuffer.py:256-287), _shell_scalar (:239-250),
 //                       _cone_scalar (:266-300), _factor_from_intensity (:197-201)
+//   pack_quads       <- repacks an externally built (n, H, W) stack
 //
-// Numerics. Everything that decides WHICH samples exist —
-// cube coverage of a texel-slice point, ray entry/exit, the float64 march
-// counter `t += step`, the inside-cube test, trilinear reconstruction, the
-// TF lookup and the alpha accumulation that drives early termination — is
-// float64 with numpy's operation order and no FMA contraction (explicit
-// __dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn), so it is bit-identical to the
-// reference. The light factor (buffer lookups for sbrc/shell/cone) is a
-// continuous function of position and runs in fp32; it only scales colour.
-// No hardware texture filtering: its 8-bit weights would break 1e-3.
+// Numerics. Everything that decides WHICH samples exist and
+// the alpha that drives early termination — cube coverage of a texel-slice
+// point, ray entry/exit, the float64 march counter `t += step`, the
+// inside-cube test, trilinear reconstruction, the TF lookup and the alpha
+// accumulation — is float64 with numpy's operation order and no FMA
+// contraction (explicit __dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn), so it is
+// bit-identical to the reference. The light factor (buffer lookups for
+// sbrc/shell/cone) is a continuous function of position and runs in fp32;
+// it only scales colour. No hardware texture filtering: its 8-bit weights
+// would break 1e-3.
+//
+// Performance notes (profiles/). The march is issue-bound,
+// not HBM-bound (L1 hit rate ~98%): the design minimises instructions per
+// sample — texel quads turn a two-layer bilinear lookup into two 16-byte
+// loads, offsets are 32-bit, edge clamping is folded into saturated
+// weights, the trilinear fetch has an unclamped interior fast path, and the
+// default cone (2 x 4) and shell (3 shells) kernels are unrolled.
 
 #include "../../include/sbrc.h"
 
@@ -35,66 +44,89 @@ __device__ __forceinline__ bool in01(double x) { return x >= 0.0 && x <= 1.0; }
 
 // ---------------------------------------------------------------- volume
 // Voxel fetch with load_raw's normalisation (volume.py:143-149): u8/u16 are
-// kept raw in HBM and normalised at fetch by an IEEE float32 division,
-// which is bit-identical to numpy's float32 `astype(float32) / 255.0`.
+// kept raw in HBM and normalised at fetch. u8 uses a 256-entry table of
+// __fdiv_rn(x, 255.f); u16 computes (float)((double)x / 65535) through a
+// double product, which rounds to the same float as the IEEE float32
+// division because x/65535 is never within 2^-40 of a float midpoint.
+// Both are bit-identical to numpy's `astype(float32) / 255.0` etc.
 template <int VT> struct Voxel;
 template <> struct Voxel<SBRC_VOXEL_F32> {
-  static __device__ __forceinline__ double get(const void* d, size_t i) {
-    return (double)__ldg(reinterpret_cast<const float*>(d) + i);
-  }
+  using T = float;
+  static __device__ __forceinline__ double cvt(float x, const float*) { return (double)x; }
 };
 template <> struct Voxel<SBRC_VOXEL_U8> {
-  static __device__ __forceinline__ double get(const void* d, size_t i) {
-    return (double)__fdiv_rn((float)__ldg(reinterpret_cast<const unsigned char*>(d) + i), 255.0f);
-  }
+  using T = unsigned char;
+  static __device__ __forceinline__ double cvt(unsigned char x, const float* tab) { return (double)tab[x]; }
 };
 template <> struct Voxel<SBRC_VOXEL_U16> {
-  static __device__ __forceinline__ double get(const void* d, size_t i) {
-    return (double)__fdiv_rn((float)__ldg(reinterpret_cast<const unsigned short*>(d) + i), 65535.0f);
+  using T = unsigned short;
+  static __device__ __forceinline__ double cvt(unsigned short x, const float*) {
+    return (double)__double2float_rn(dmul((double)x, 1.0 / 65535.0));
   }
 };
 
 // Cell-centred trilinear reconstruction, clamp-to-edge, 0 outside the unit
-// cube: sample_trilinear_many (volume.py:161-194), same op order.
+// cube: sample_trilinear_many (volume.py:161-194), same op order. The
+// voxel index is 32-bit (validated: nx*ny*nz < 2^32).
 template <int VT>
-__device__ __forceinline__ double trilinear64(const sbrc_volume& v, double px, double py, double pz) {
+__device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float* u8tab, double px, double py,
+                                              double pz) {
+  using T = typename Voxel<VT>::T;
   if (!(in01(px) && in01(py) && in01(pz))) return 0.0;
-  double p[3] = {px, py, pz};
+  const double p[3] = {px, py, pz};
   const int dims[3] = {v.nx, v.ny, v.nz};
-  int i0[3], i1[3];
+  int lo[3];
   double f[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     double local = dsub(p[c], v.box_lo[c]);
     if (v.box_ext[c] != 1.0) local = ddiv(local, v.box_ext[c]);  // x/1.0 == x exactly
     local = dclip01(local);
-    double g = dsub(dmul(local, (double)dims[c]), 0.5);
-    double fl = floor(g);
+    const double g = dsub(dmul(local, (double)dims[c]), 0.5);
+    const double fl = floor(g);
     f[c] = dsub(g, fl);
-    int lo = (int)fl;
-    i0[c] = min(max(lo, 0), dims[c] - 1);
-    i1[c] = min(max(lo + 1, 0), dims[c] - 1);
+    lo[c] = (int)fl;
   }
-  const size_t sx = 1, sy = (size_t)v.nx, sz = (size_t)v.nx * (size_t)v.ny;
-  const size_t bz0 = (size_t)i0[2] * sz, bz1 = (size_t)i1[2] * sz;
-  const size_t by0 = (size_t)i0[1] * sy, by1 = (size_t)i1[1] * sy;
-  const size_t x0 = (size_t)i0[0] * sx, x1 = (size_t)i1[0] * sx;
-  const double d000 = Voxel<VT>::get(v.data, bz0 + by0 + x0);
-  const double d100 = Voxel<VT>::get(v.data, bz0 + by0 + x1);
-  const double d010 = Voxel<VT>::get(v.data, bz0 + by1 + x0);
-  const double d110 = Voxel<VT>::get(v.data, bz0 + by1 + x1);
-  const double d001 = Voxel<VT>::get(v.data, bz1 + by0 + x0);
-  const double d101 = Voxel<VT>::get(v.data, bz1 + by0 + x1);
-  const double d011 = Voxel<VT>::get(v.data, bz1 + by1 + x0);
-  const double d111 = Voxel<VT>::get(v.data, bz1 + by1 + x1);
+  const T* base = reinterpret_cast<const T*>(v.data);
+  const unsigned nx = (unsigned)v.nx, nxy = (unsigned)v.nx * (unsigned)v.ny;
+  T r000, r100, r010, r110, r001, r101, r011, r111;
+  if (lo[0] >= 0 && lo[0] < v.nx - 1 && lo[1] >= 0 && lo[1] < v.ny - 1 && lo[2] >= 0 && lo[2] < v.nz - 1) {
+    // interior: the 2x2x2 cell without clamping
+    const T* c = base + ((unsigned)lo[0] + nx * (unsigned)lo[1] + nxy * (unsigned)lo[2]);
+    const T* cy = c + nx;
+    const T* cz = c + nxy;
+    const T* cyz = cz + nx;
+    r000 = __ldg(c); r100 = __ldg(c + 1); r010 = __ldg(cy); r110 = __ldg(cy + 1);
+    r001 = __ldg(cz); r101 = __ldg(cz + 1); r011 = __ldg(cyz); r111 = __ldg(cyz + 1);
+  } else {
+    // faces: i0 = clip(lo), i1 = clip(lo + 1) (volume.py:180-182)
+    unsigned a[3], b[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      a[c] = (unsigned)min(max(lo[c], 0), dims[c] - 1);
+      b[c] = (unsigned)min(max(lo[c] + 1, 0), dims[c] - 1);
+    }
+    const unsigned z0 = a[2] * nxy, z1 = b[2] * nxy, y0 = a[1] * nx, y1 = b[1] * nx;
+    r000 = __ldg(base + (z0 + y0 + a[0])); r100 = __ldg(base + (z0 + y0 + b[0]));
+    r010 = __ldg(base + (z0 + y1 + a[0])); r110 = __ldg(base + (z0 + y1 + b[0]));
+    r001 = __ldg(base + (z1 + y0 + a[0])); r101 = __ldg(base + (z1 + y0 + b[0]));
+    r011 = __ldg(base + (z1 + y1 + a[0])); r111 = __ldg(base + (z1 + y1 + b[0]));
+  }
+  using V = Voxel<VT>;
   const double gx = dsub(1.0, f[0]), gy = dsub(1.0, f[1]), gz = dsub(1.0, f[2]);
-  const double c00 = dadd(dmul(d000, gx), dmul(d100, f[0]));
-  const double c10 = dadd(dmul(d010, gx), dmul(d110, f[0]));
-  const double c01 = dadd(dmul(d001, gx), dmul(d101, f[0]));
-  const double c11 = dadd(dmul(d011, gx), dmul(d111, f[0]));
+  const double c00 = dadd(dmul(V::cvt(r000, u8tab), gx), dmul(V::cvt(r100, u8tab), f[0]));
+  const double c10 = dadd(dmul(V::cvt(r010, u8tab), gx), dmul(V::cvt(r110, u8tab), f[0]));
+  const double c01 = dadd(dmul(V::cvt(r001, u8tab), gx), dmul(V::cvt(r101, u8tab), f[0]));
+  const double c11 = dadd(dmul(V::cvt(r011, u8tab), gx), dmul(V::cvt(r111, u8tab), f[0]));
   const double c0 = dadd(dmul(c00, gy), dmul(c10, f[1]));
   const double c1 = dadd(dmul(c01, gy), dmul(c11, f[1]));
   return dadd(dmul(c0, gz), dmul(c1, f[2]));
+}
+
+// u8 normalisation table: tab[x] = (float)x / 255.0f, IEEE division.
+__device__ __forceinline__ void fill_u8_table(float* tab) {
+  for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < 256; i += blockDim.x * blockDim.y)
+    tab[i] = __fdiv_rn((float)i, 255.0f);
 }
 
 // LUT position: t = clip(s,0,1)*255, i0 = floor(t) (truncation, s >= 0),
@@ -114,16 +146,30 @@ __device__ __forceinline__ LutPos lut_pos(double s) {
   return r;
 }
 
+// ---------------------------------------------------------------- texel quads
+// Quad (k, y, x) = (I[k][y][x], I[k+][y][x], I[k][y][x+], I[k+][y][x+]).
+// Writing texel x's pair (I[k], I[k+]) fills .xy of quad x and .zw of quad
+// x-1 (and .zw of quad x at the right edge, where x+ = x).
+__device__ __forceinline__ void emit_pair(float4* row, int x, int w, float a, float b) {
+  float2* r2 = reinterpret_cast<float2*>(row);
+  r2[2 * x] = make_float2(a, b);
+  if (x > 0) r2[2 * x - 1] = make_float2(a, b);
+  if (x == w - 1) r2[2 * x + 1] = make_float2(a, b);
+}
+
 // ---------------------------------------------------------------- K1 build
 // One thread per light texel; the slice recurrence runs in registers
 // (lightbuffer.py:166-198): intensity[k] = T; if the texel-slice point is in
 // the cube, alpha = lut(trilinear(p)) and T *= 1 - alpha. Texels are
-// independent, so no grid-wide barrier or per-slice launch is needed.
+// independent, so no grid-wide barrier or per-slice launch is needed. The
+// quad of layer k needs layer k+1, so it is emitted one slice late.
 template <int VT>
 __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   __shared__ double lut[SBRC_LUT_SIZE];
+  __shared__ float u8tab[256];
   for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x * blockDim.y)
     lut[i] = P.alpha_lut[i];
+  if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
   __syncthreads();
 
   const sbrc_light_frame& L = P.light;
@@ -143,8 +189,10 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   for (int c = 0; c < 3; ++c) base[c] = dadd(dmul(uc, L.axis_u[c]), dmul(vc, L.axis_v[c]));
 
   const bool comp = P.compensation_n > 0.0;
-  float* out = P.out + (size_t)(y - P.row_begin) * (size_t)P.row_stride + (size_t)x;
+  float4* row = reinterpret_cast<float4*>(P.quads) + (size_t)(y - P.row_begin) * (size_t)P.quad_row_stride;
+  const size_t ks = (size_t)P.quad_layer_stride;
   double T = 1.0;
+  float prev = 0.0f;
   for (int k = 0; k < L.n_slices; ++k) {
     const double off = __ldg(L.plane_offsets + k);
     // pts = base + offset_k * L (:182); covered = all(0 <= pts <= 1) (:183)
@@ -153,85 +201,108 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
     const double pz = dadd(base[2], dmul(off, L.light_dir[2]));
     float stored = (float)T;  // intensity[k] = trans (:169)
     if (in01(px) && in01(py) && in01(pz)) {
-      const double s = trilinear64<VT>(P.volume, px, py, pz);
+      const double s = trilinear64<VT>(P.volume, u8tab, px, py, pz);
       const LutPos q = lut_pos(s);
       const double a = dadd(dmul(lut[q.i0], q.g), dmul(lut[q.i1], q.f));
       if (comp) stored = (float)dmul((double)stored, pow(dadd(1.0, a), P.compensation_n));  // :193-196
       T = dmul(T, dsub(1.0, a));  // :197-198
     }
-    out[(size_t)k * (size_t)P.layer_stride] = stored;
+    if (k > 0) emit_pair(row + (size_t)(k - 1) * ks, x, L.width, prev, stored);
+    prev = stored;
   }
+  emit_pair(row + (size_t)(L.n_slices - 1) * ks, x, L.width, prev, prev);
+}
+
+// Repack a plain stack into quads (one thread per texel, loop over layers).
+__global__ void __launch_bounds__(256) pack_quads_kernel(const float* __restrict__ plain, int64_t pk, int64_t py,
+                                                         int n, int h, int w, float* quads, int64_t qk,
+                                                         int64_t qy) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= w || y >= h) return;
+  const float* src = plain + (size_t)y * (size_t)py + (size_t)x;
+  float4* row = reinterpret_cast<float4*>(quads) + (size_t)y * (size_t)qy;
+  float prev = __ldg(src);
+  for (int k = 1; k < n; ++k) {
+    const float cur = __ldg(src + (size_t)k * (size_t)pk);
+    emit_pair(row + (size_t)(k - 1) * (size_t)qk, x, w, prev, cur);
+    prev = cur;
+  }
+  emit_pair(row + (size_t)(n - 1) * (size_t)qk, x, w, prev, prev);
 }
 
 // ---------------------------------------------------------------- K2 march
-struct LightTex {
-  const float* I;
-  size_t ks, ys;  // layer and row strides (elements)
-  int W, H, n;
-  float fW, fH, fnm1;
+// Light-space lookup state. Texel coordinates tx = u*W - 0.5, ty = v*H - 0.5
+// and the layer coordinate li = idx - 0.5 (lightbuffer.py:241-242, :279).
+struct QuadTex {
+  const float4* q;
+  unsigned qk, qy, qy1;  // layer / row strides in quads; qy1 = row step to y+1 (0 if H == 1)
+  float txmax, tymax;    // footprint: u in [0,1]  <=>  tx in [-0.5, W-0.5]
+  float xa_max, ya_max;  // max(W-2, 0), max(H-2, 0)
+  float li_max, ka_max;  // n-1, max(n-2, 0)
 };
 
-// Clamp-to-edge bilinear inside one layer (_bilinear_layers, lightbuffer.py:238-253).
-__device__ __forceinline__ float bilinear_layer(const float* layer, size_t ys, float fx, float fy,
-                                                int x0c, int x1c, int y0c, int y1c) {
-  const float* r0 = layer + (size_t)y0c * ys;
-  const float* r1 = layer + (size_t)y1c * ys;
-  const float c0 = __ldg(r0 + x0c) * (1.0f - fx) + __ldg(r0 + x1c) * fx;
-  const float c1 = __ldg(r1 + x0c) * (1.0f - fx) + __ldg(r1 + x1c) * fx;
-  return c0 * (1.0f - fy) + c1 * fy;
-}
+__device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b, fmaf(-t, a, a)); }
 
-// lookup_light_scalar_many at one light-space position (u, v, idx): outside
-// the footprint -> 1 (:268-269); linear: plane k sits at continuous index
-// k+0.5, blend the two bracketing layers (:277-285); nearest: one layer (:274-276).
+// lookup_light_scalar_many at one point (lightbuffer.py:256-287): 1 outside
+// the footprint (:268-269); linear: bilinear in the two layers bracketing
+// plane-centred coordinate li, blended (:277-285); nearest: one layer
+// (:274-276). Index clamping (clip(x0,0,W-1), clip(x0+1,0,W-1)) is replaced
+// by clamping the cell to [0, W-2] and saturating the weight, which selects
+// the same texel values.
 template <int LOOKUP>
-__device__ __forceinline__ float light_lookup(const LightTex& t, float u, float v, float idx) {
-  if (!(u >= 0.0f && u <= 1.0f && v >= 0.0f && v <= 1.0f)) return 1.0f;
-  const float tx = u * t.fW - 0.5f, ty = v * t.fH - 0.5f;
-  const float flx = floorf(tx), fly = floorf(ty);
-  const float fx = tx - flx, fy = ty - fly;
-  const int x0 = (int)flx, y0 = (int)fly;  // >= -1 and <= W-1 inside the footprint
-  const int x0c = max(x0, 0), x1c = min(x0 + 1, t.W - 1);
-  const int y0c = max(y0, 0), y1c = min(y0 + 1, t.H - 1);
+__device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float ty, float li_raw) {
+  // li_raw: idx - 0.5 for linear lookups, idx for nearest
+  if (!(tx >= -0.5f && tx <= t.txmax && ty >= -0.5f && ty <= t.tymax)) return 1.0f;
+  const float xa = fminf(fmaxf(floorf(tx), 0.0f), t.xa_max);
+  const float ya = fminf(fmaxf(floorf(ty), 0.0f), t.ya_max);
+  const float fx = __saturatef(tx - xa), fy = __saturatef(ty - ya);
+  float ka, f;
   if (LOOKUP == SBRC_LOOKUP_NEAREST) {
-    const int k = min((int)floorf(fminf(fmaxf(idx, 0.0f), t.fnm1)), t.n - 1);
-    return bilinear_layer(t.I + (size_t)k * t.ks, t.ys, fx, fy, x0c, x1c, y0c, y1c);
+    // k = floor(clip(idx, 0, n-1)) (:275); for nearest lookups li_raw is idx
+    ka = floorf(fminf(fmaxf(li_raw, 0.0f), t.li_max));
+    f = 0.0f;
   } else {
-    const float li = fminf(fmaxf(idx - 0.5f, 0.0f), t.fnm1);
-    const int k0 = min((int)li, t.n - 1);
-    const int k1 = min(k0 + 1, t.n - 1);
-    const float f = li - (float)k0;
-    const float v0 = bilinear_layer(t.I + (size_t)k0 * t.ks, t.ys, fx, fy, x0c, x1c, y0c, y1c);
-    const float v1 = bilinear_layer(t.I + (size_t)k1 * t.ks, t.ys, fx, fy, x0c, x1c, y0c, y1c);
-    return v0 * (1.0f - f) + v1 * f;
+    const float li = fminf(fmaxf(li_raw, 0.0f), t.li_max);
+    ka = fminf(floorf(li), t.ka_max);
+    f = li - ka;
   }
+  const unsigned off = (unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa;
+  const float4 r0 = __ldg(t.q + off);
+  const float4 r1 = __ldg(t.q + off + t.qy1);
+  const float a0 = lerpf(r0.x, r0.z, fx), a1 = lerpf(r1.x, r1.z, fx);  // layer ka, rows y, y+1
+  const float v0 = lerpf(a0, a1, fy);
+  if (LOOKUP == SBRC_LOOKUP_NEAREST) return v0;
+  const float b0 = lerpf(r0.y, r0.w, fx), b1 = lerpf(r1.y, r1.w, fx);  // layer ka+1
+  return lerpf(v0, lerpf(b0, b1, fy), f);
 }
 
 struct ShellTap {
-  float du, dv, di, w;  // light-space offset of +radius along one world axis
+  float dtx, dty, dli, w;  // texel-space offset of +radius along one world axis; shell weight
 };
 
-template <int SHADING, int LOOKUP, int VT>
+template <int SHADING, int LOOKUP, int VT, int NSHELL, int CONE_A, int CONE_N>
 __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) {
   __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
+  __shared__ float u8tab[256];
   for (int i = threadIdx.x; i < SBRC_LUT_SIZE * 2; i += blockDim.x)
     lut[i] = reinterpret_cast<const double2*>(P.lut_rgba)[i];
+  if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
 
   const sbrc_light_frame& LF = P.light;
-  // Per-frame light-space constants: u = (p.au - u0)/(u1-u0), v likewise,
-  // idx = n (p.L - d_min)/(d_max - d_min) (world_to_light_uv_many :202-212,
-  // slice_index_many slicing.py:101-105).
-  const double su = 1.0 / (LF.u_range[1] - LF.u_range[0]);
-  const double sv = 1.0 / (LF.v_range[1] - LF.v_range[0]);
+  // Light space (world_to_light_uv_many :202-212, slice_index_many slicing.py:101-105):
+  // tx = ((p.au - u0)/(u1-u0))*W - 0.5, ty likewise, li = n (p.L - d_min)/(d_max - d_min) - 0.5.
+  const double sx = (double)LF.width / (LF.u_range[1] - LF.u_range[0]);
+  const double sy = (double)LF.height / (LF.v_range[1] - LF.v_range[0]);
   const double si = (double)LF.n_slices / (LF.d_max - LF.d_min);
   if (SHADING == SBRC_SHADE_SHELL) {
-    // p +- r e_a maps to (u,v,idx) +- r (au[a] su, av[a] sv, L[a] si).
+    // p +- r e_a maps to (tx, ty, li) +- r (au[a] sx, av[a] sy, L[a] si).
     for (int i = threadIdx.x; i < P.shell_count * 3; i += blockDim.x) {
       const int s = i / 3, a = i % 3;
       const double r = P.shell_radius[s];
-      shell_taps[i] = ShellTap{(float)(r * LF.axis_u[a] * su), (float)(r * LF.axis_v[a] * sv),
+      shell_taps[i] = ShellTap{(float)(r * LF.axis_u[a] * sx), (float)(r * LF.axis_v[a] * sy),
                                (float)(r * LF.light_dir[a] * si), (float)P.shell_weight[s]};
     }
   }
@@ -251,6 +322,7 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
   const bool valid = in_image && py < P.height;
 
   unsigned int samples = 0;
+  float4 result = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
     // ---- Camera.rays (raycaster.py:53-68), numpy op order, float64.
     const double ndc_x = dmul(dmul(dsub(dmul(ddiv(dadd((double)px, 0.5), (double)P.width), 2.0), 1.0),
@@ -283,20 +355,22 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
     const double t_enter = fmax(t_near, 0.0);
 
     if (t_far > t_enter) {
-      LightTex tex;
-      tex.I = P.intensity;
-      tex.ks = (size_t)P.layer_stride;
-      tex.ys = (size_t)P.row_stride;
-      tex.W = LF.width;
-      tex.H = LF.height;
-      tex.n = LF.n_slices;
-      tex.fW = (float)LF.width;
-      tex.fH = (float)LF.height;
-      tex.fnm1 = (float)(LF.n_slices - 1);
-      // Light-space coordinates are affine in t along the ray.
-      double lu0 = 0, lud = 0, lv0 = 0, lvd = 0, li0 = 0, lid = 0;
+      QuadTex tex;
+      // Light-space coordinates are affine in t along the ray: c(t) = c0 + t*cd.
+      double tx0 = 0, txd = 0, ty0 = 0, tyd = 0, li0 = 0, lid = 0;
       float cbu = 1.0f, cbv = 0.0f, dperp = 0.0f;
+      float fr_c = 1.f, fg_c = 1.f, fb_c = 1.f, ir = 1.f, ig = 1.f, ib = 1.f;
       if (SHADING != SBRC_SHADE_NONE) {
+        tex.q = reinterpret_cast<const float4*>(P.quads);
+        tex.qk = (unsigned)P.quad_layer_stride;
+        tex.qy = (unsigned)P.quad_row_stride;
+        tex.qy1 = LF.height > 1 ? tex.qy : 0u;
+        tex.txmax = (float)LF.width - 0.5f;
+        tex.tymax = (float)LF.height - 0.5f;
+        tex.xa_max = (float)max(LF.width - 2, 0);
+        tex.ya_max = (float)max(LF.height - 2, 0);
+        tex.li_max = (float)(LF.n_slices - 1);
+        tex.ka_max = (float)max(LF.n_slices - 2, 0);
         double eu = 0, ev = 0, el = 0, du_ = 0, dv_ = 0, dl_ = 0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -307,23 +381,44 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
           dv_ += d[c] * LF.axis_v[c];
           dl_ += d[c] * LF.light_dir[c];
         }
-        lu0 = (eu - LF.u_range[0]) * su;
-        lud = du_ * su;
-        lv0 = (ev - LF.v_range[0]) * sv;
-        lvd = dv_ * sv;
-        li0 = (el - LF.d_min) * si;
+        tx0 = (eu - LF.u_range[0]) * sx - 0.5;
+        txd = du_ * sx;
+        ty0 = (ev - LF.v_range[0]) * sy - 0.5;
+        tyd = dv_ * sy;
+        // linear lookups use the plane-centred li = idx - 0.5; nearest uses idx itself
+        li0 = (el - LF.d_min) * si - (LOOKUP == SBRC_LOOKUP_NEAREST ? 0.0 : 0.5);
         lid = dl_ * si;
         if (SHADING == SBRC_SHADE_CONE) {
           // Ring basis: normalize(e - (e.L)L) with e = eye - p = -t d, so it is
           // -d_perp/|d_perp| for the whole ray (raycaster.py:276-282); its
           // in-plane coordinates are (-du_, -dv_)/|d_perp|.
-          const double pu = -du_, pv = -dv_;
-          const double pn = sqrt(pu * pu + pv * pv);
+          const double pn = sqrt(du_ * du_ + dv_ * dv_);
           dperp = (float)pn;
           if (pn > 0.0) {
-            cbu = (float)(pu / pn);
-            cbv = (float)(pv / pn);
+            cbu = (float)(-du_ / pn);
+            cbv = (float)(-dv_ / pn);
           }
+        }
+        // _factor_from_intensity (raycaster.py:197-201): max(s*c, floor)/c, 1 where c == 0
+        fr_c = P.light_color[0];
+        fg_c = P.light_color[1];
+        fb_c = P.light_color[2];
+        ir = fr_c > 0.f ? 1.0f / fr_c : 0.f;
+        ig = fg_c > 0.f ? 1.0f / fg_c : 0.f;
+        ib = fb_c > 0.f ? 1.0f / fb_c : 0.f;
+      }
+      // Cone ring geometry per ray (texel units): tap (i, j) sits at
+      // (tx + r_i*wx_j, ty + r_i*wy_j, li - i), r_i = ring * i * spacing.
+      constexpr int NA = CONE_N > 0 ? CONE_N : 1;
+      float wx[NA], wy[NA];
+      const float spacing_r = (float)(P.cone_ring * ((LF.d_max - LF.d_min) / LF.n_slices));
+      float bu_fb = cbu, bv_fb = cbv;
+      if (SHADING == SBRC_SHADE_CONE && CONE_N > 0) {
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+          const float c = (float)P.cone_cos[j], s = (float)P.cone_sin[j];
+          wx[j] = (float)sx * (cbu * c - cbv * s);
+          wy[j] = (float)sy * (cbv * c + cbu * s);
         }
       }
       const double step = P.step, thresh = P.et_alpha;
@@ -335,7 +430,7 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
         const double qx = dadd(P.eye[0], dmul(t, d[0]));
         const double qy = dadd(P.eye[1], dmul(t, d[1]));
         const double qz = dadd(P.eye[2], dmul(t, d[2]));
-        const double s = trilinear64<VT>(P.volume, qx, qy, qz);
+        const double s = trilinear64<VT>(P.volume, u8tab, qx, qy, qz);
         const LutPos q = lut_pos(s);
         const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
         const double2 b_rg = lut[2 * q.i1], b_ba = lut[2 * q.i1 + 1];
@@ -344,70 +439,83 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
         const double sb = dadd(dmul(a_ba.x, q.g), dmul(b_ba.x, q.f));
         const double sa = dadd(dmul(a_ba.y, q.g), dmul(b_ba.y, q.f));
 
-        float fr = 1.0f, fg = 1.0f, fb = 1.0f;
+        double fr = 1.0, fg = 1.0, fb = 1.0;
         if (SHADING != SBRC_SHADE_NONE) {
-          const float u = (float)(lu0 + t * lud);
-          const float v = (float)(lv0 + t * lvd);
-          const float idx = (float)(li0 + t * lid);
+          const float tx = (float)fma(t, txd, tx0);
+          const float ty = (float)fma(t, tyd, ty0);
+          const float li = (float)fma(t, lid, li0);
           float scalar;
           if (SHADING == SBRC_SHADE_SHADOW) {
-            scalar = light_lookup<LOOKUP>(tex, u, v, idx);
+            scalar = light_lookup<LOOKUP>(tex, tx, ty, li);
           } else if (SHADING == SBRC_SHADE_SHELL) {
             float acc = 0.0f;
-            for (int sh = 0; sh < P.shell_count; ++sh) {
+            const int nsh = NSHELL > 0 ? NSHELL : P.shell_count;
+#pragma unroll
+            for (int sh = 0; sh < (NSHELL > 0 ? NSHELL : SBRC_MAX_SHELLS); ++sh) {
+              if (NSHELL == 0 && sh >= nsh) break;
               float shell = 0.0f;
 #pragma unroll
               for (int a = 0; a < 3; ++a) {
                 const ShellTap tp = shell_taps[sh * 3 + a];
-                shell += light_lookup<LOOKUP>(tex, u + tp.du, v + tp.dv, idx + tp.di);
-                shell += light_lookup<LOOKUP>(tex, u - tp.du, v - tp.dv, idx - tp.di);
+                shell += light_lookup<LOOKUP>(tex, tx + tp.dtx, ty + tp.dty, li + tp.dli);
+                shell += light_lookup<LOOKUP>(tex, tx - tp.dtx, ty - tp.dty, li - tp.dli);
               }
               acc += shell_taps[sh * 3].w * shell / 6.0f;
             }
             scalar = acc;
           } else {  // cone
-            float bu = cbu, bv = cbv;
-            if (!((double)dperp * t > 1e-12)) {  // fallback plane_basis(L)[0] = axis_u
-              bu = 1.0f;
-              bv = 0.0f;
-            }
+            const bool degenerate = !((double)dperp * t > 1e-12);  // fallback plane_basis(L)[0] = axis_u
             float acc = 0.0f;
-            for (int i = 1; i <= P.cone_axis_samples; ++i) {
-              const float r = (float)(P.cone_ring * (double)i * ((LF.d_max - LF.d_min) / LF.n_slices));
-              const float ru = r * (float)su, rv = r * (float)sv;
-              const float ki = idx - (float)i;
-              for (int j = 0; j < P.cone_angle_count; ++j) {
-                const float2 cs = cone_cs[j];
-                const float wu = bu * cs.x - bv * cs.y;
-                const float wv = bv * cs.x + bu * cs.y;
-                acc += light_lookup<LOOKUP>(tex, u + ru * wu, v + rv * wv, ki);
+            if (CONE_N > 0) {
+#pragma unroll
+              for (int i = 1; i <= CONE_A; ++i) {
+                const float r = spacing_r * (float)i;
+                const float ki = li - (float)i;
+#pragma unroll
+                for (int j = 0; j < NA; ++j) {
+                  float ox = r * wx[j], oy = r * wy[j];
+                  if (degenerate) {
+                    const float c = cone_cs[j].x, sn = cone_cs[j].y;
+                    ox = r * (float)sx * c;
+                    oy = r * (float)sy * sn;
+                  }
+                  acc += light_lookup<LOOKUP>(tex, tx + ox, ty + oy, ki);
+                }
               }
+              scalar = acc * (1.0f / (float)(CONE_A * NA));
+            } else {
+              const float bu = degenerate ? 1.0f : bu_fb, bv = degenerate ? 0.0f : bv_fb;
+              for (int i = 1; i <= P.cone_axis_samples; ++i) {
+                const float r = spacing_r * (float)i;
+                const float ki = li - (float)i;
+                for (int j = 0; j < P.cone_angle_count; ++j) {
+                  const float2 cs = cone_cs[j];
+                  const float ox = r * (float)sx * (bu * cs.x - bv * cs.y);
+                  const float oy = r * (float)sy * (bv * cs.x + bu * cs.y);
+                  acc += light_lookup<LOOKUP>(tex, tx + ox, ty + oy, ki);
+                }
+              }
+              scalar = acc / (float)(P.cone_axis_samples * P.cone_angle_count);
             }
-            scalar = acc / (float)(P.cone_axis_samples * P.cone_angle_count);
           }
-          // _factor_from_intensity (raycaster.py:197-201)
-          const float c0 = P.light_color[0], c1 = P.light_color[1], c2 = P.light_color[2];
-          fr = c0 > 0.0f ? fmaxf(scalar * c0, P.ambient_floor) / c0 : 1.0f;
-          fg = c1 > 0.0f ? fmaxf(scalar * c1, P.ambient_floor) / c1 : 1.0f;
-          fb = c2 > 0.0f ? fmaxf(scalar * c2, P.ambient_floor) / c2 : 1.0f;
+          fr = fr_c > 0.f ? (double)(fmaxf(scalar * fr_c, P.ambient_floor) * ir) : 1.0;
+          fg = fg_c > 0.f ? (double)(fmaxf(scalar * fg_c, P.ambient_floor) * ig) : 1.0;
+          fb = fb_c > 0.f ? (double)(fmaxf(scalar * fb_c, P.ambient_floor) * ib) : 1.0;
         }
         // C += (1-a)*rgb*factor; a += (1-a)*a_src (raycaster.py:436-438)
         const double one_m = dsub(1.0, alpha);
-        cr = dadd(cr, dmul(dmul(one_m, sr), (double)fr));
-        cg = dadd(cg, dmul(dmul(one_m, sg), (double)fg));
-        cb = dadd(cb, dmul(dmul(one_m, sb), (double)fb));
+        cr = dadd(cr, dmul(dmul(one_m, sr), fr));
+        cg = dadd(cg, dmul(dmul(one_m, sg), fg));
+        cb = dadd(cb, dmul(dmul(one_m, sb), fb));
         alpha = dadd(alpha, dmul(one_m, sa));
         t = dadd(t, step);
         ++samples;
       }
-      float4* out = reinterpret_cast<float4*>(P.image) + (size_t)lr * P.width + px;
-      *out = make_float4((float)cr, (float)cg, (float)cb, (float)alpha);
-    } else {
-      reinterpret_cast<float4*>(P.image)[(size_t)lr * P.width + px] = make_float4(0.f, 0.f, 0.f, 0.f);
+      result = make_float4((float)cr, (float)cg, (float)cb, (float)alpha);
     }
-  } else if (in_image) {  // padding row of a partial last band
-    reinterpret_cast<float4*>(P.image)[(size_t)lr * P.width + px] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  if (in_image)  // background (and padding rows of a partial last band) is transparent black
+    reinterpret_cast<float4*>(P.image)[(size_t)lr * P.width + px] = result;
   if (P.sample_count != nullptr) {
     const unsigned int tot = __reduce_add_sync(0xffffffffu, samples);
     if (lane == 0 && tot) atomicAdd(P.sample_count, (unsigned long long)tot);
@@ -418,6 +526,7 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
 bool volume_ok(const sbrc_volume& v) {
   if (v.data == nullptr) return false;
   if (v.nx < 2 || v.ny < 2 || v.nz < 2) return false;  // volume.py:80-81
+  if ((unsigned long long)v.nx * v.ny * v.nz >= (1ull << 32)) return false;  // 32-bit voxel offsets
   if (v.voxel_type < SBRC_VOXEL_F32 || v.voxel_type > SBRC_VOXEL_U16) return false;
   for (int c = 0; c < 3; ++c)
     if (!(v.box_ext[c] > 0.0)) return false;
@@ -429,6 +538,13 @@ bool light_ok(const sbrc_light_frame& L) {
          L.u_range[1] > L.u_range[0] && L.v_range[1] > L.v_range[0];
 }
 
+// Largest quad offset must fit 32 bits (K2 addresses quads with 32-bit offsets).
+bool quads_ok(const sbrc_light_frame& L, int64_t qk, int64_t qy) {
+  if (qk < 1 || qy < L.width) return false;
+  const long long last = (long long)(L.n_slices - 1) * qk + (long long)(L.height - 1) * qy + L.width;
+  return last < (1ll << 32);
+}
+
 template <int VT>
 void launch_build(const sbrc_build_params& p, cudaStream_t s) {
   dim3 block(32, 8);
@@ -436,24 +552,37 @@ void launch_build(const sbrc_build_params& p, cudaStream_t s) {
   build_kernel<VT><<<grid, block, 0, s>>>(p);
 }
 
-template <int SH, int LK, int VT>
-void launch_march3(const sbrc_render_params& p, cudaStream_t s) {
+template <int SH, int LK, int VT, int NS, int CA, int CN>
+void launch_march(const sbrc_render_params& p, cudaStream_t s) {
   const int rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
   dim3 grid((p.width + 31) / 32, (rows + 7) / 8);
-  march_kernel<SH, LK, VT><<<grid, 256, 0, s>>>(p);
+  march_kernel<SH, LK, VT, NS, CA, CN><<<grid, 256, 0, s>>>(p);
+}
+
+template <int SH, int LK, int VT>
+void launch_march_kernel_shape(const sbrc_render_params& p, cudaStream_t s) {
+  if (SH == SBRC_SHADE_SHELL) {
+    if (p.shell_count == 3) launch_march<SH, LK, VT, 3, 0, 0>(p, s);
+    else launch_march<SH, LK, VT, 0, 0, 0>(p, s);
+  } else if (SH == SBRC_SHADE_CONE) {
+    if (p.cone_axis_samples == 2 && p.cone_angle_count == 4) launch_march<SH, LK, VT, 0, 2, 4>(p, s);
+    else launch_march<SH, LK, VT, 0, 0, 0>(p, s);
+  } else {
+    launch_march<SH, LK, VT, 0, 0, 0>(p, s);
+  }
 }
 template <int SH, int LK>
-void launch_march2(const sbrc_render_params& p, cudaStream_t s) {
+void launch_march_vt(const sbrc_render_params& p, cudaStream_t s) {
   switch (p.volume.voxel_type) {
-    case SBRC_VOXEL_F32: launch_march3<SH, LK, SBRC_VOXEL_F32>(p, s); break;
-    case SBRC_VOXEL_U8: launch_march3<SH, LK, SBRC_VOXEL_U8>(p, s); break;
-    default: launch_march3<SH, LK, SBRC_VOXEL_U16>(p, s); break;
+    case SBRC_VOXEL_F32: launch_march_kernel_shape<SH, LK, SBRC_VOXEL_F32>(p, s); break;
+    case SBRC_VOXEL_U8: launch_march_kernel_shape<SH, LK, SBRC_VOXEL_U8>(p, s); break;
+    default: launch_march_kernel_shape<SH, LK, SBRC_VOXEL_U16>(p, s); break;
   }
 }
 template <int SH>
-void launch_march1(const sbrc_render_params& p, cudaStream_t s) {
-  if (p.lookup == SBRC_LOOKUP_NEAREST) launch_march2<SH, SBRC_LOOKUP_NEAREST>(p, s);
-  else launch_march2<SH, SBRC_LOOKUP_LINEAR>(p, s);
+void launch_march_lookup(const sbrc_render_params& p, cudaStream_t s) {
+  if (SH != SBRC_SHADE_NONE && p.lookup == SBRC_LOOKUP_NEAREST) launch_march_vt<SH, SBRC_LOOKUP_NEAREST>(p, s);
+  else launch_march_vt<SH, SBRC_LOOKUP_LINEAR>(p, s);
 }
 
 }  // namespace
@@ -494,9 +623,9 @@ int sbrc_local_rows(int height, int band_rows, int rank, int world) {
 
 int sbrc_build(const sbrc_build_params* p, void* stream) {
   if (p == nullptr || !volume_ok(p->volume) || !light_ok(p->light)) return SBRC_EINVAL;
-  if (p->light.plane_offsets == nullptr || p->alpha_lut == nullptr || p->out == nullptr) return SBRC_EINVAL;
+  if (p->light.plane_offsets == nullptr || p->alpha_lut == nullptr || p->quads == nullptr) return SBRC_EINVAL;
   if (p->row_begin < 0 || p->row_end > p->light.height || p->row_begin >= p->row_end) return SBRC_EINVAL;
-  if (p->layer_stride < 1 || p->row_stride < p->light.width) return SBRC_EINVAL;
+  if (p->quad_layer_stride < 1 || p->quad_row_stride < p->light.width) return SBRC_EINVAL;
   if (p->compensation_n < 0.0) return SBRC_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (p->volume.voxel_type) {
@@ -504,6 +633,19 @@ int sbrc_build(const sbrc_build_params* p, void* stream) {
     case SBRC_VOXEL_U8: launch_build<SBRC_VOXEL_U8>(*p, s); break;
     default: launch_build<SBRC_VOXEL_U16>(*p, s); break;
   }
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_pack_quads(const float* plain, int64_t plain_layer_stride, int64_t plain_row_stride, int n, int height,
+                    int width, float* quads, int64_t quad_layer_stride, int64_t quad_row_stride, void* stream) {
+  if (plain == nullptr || quads == nullptr || n < 1 || height < 1 || width < 1) return SBRC_EINVAL;
+  if (plain_layer_stride < 1 || plain_row_stride < width || quad_layer_stride < 1 || quad_row_stride < width)
+    return SBRC_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  dim3 block(32, 8);
+  dim3 grid((width + 31) / 32, (height + 7) / 8);
+  pack_quads_kernel<<<grid, block, 0, s>>>(plain, plain_layer_stride, plain_row_stride, n, height, width, quads,
+                                           quad_layer_stride, quad_row_stride);
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 
@@ -517,9 +659,9 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
   if (p->band_rows < 1 || p->band_rows % 8 != 0 || p->world < 1 || p->rank < 0 || p->rank >= p->world)
     return SBRC_EINVAL;
   if (p->shading != SBRC_SHADE_NONE) {
-    if (p->intensity == nullptr) return SBRC_ECONFIG;
+    if (p->quads == nullptr) return SBRC_ECONFIG;
     if (!light_ok(p->light)) return SBRC_EINVAL;
-    if (p->layer_stride < 1 || p->row_stride < p->light.width) return SBRC_EINVAL;
+    if (!quads_ok(p->light, p->quad_layer_stride, p->quad_row_stride)) return SBRC_EINVAL;
   }
   if (p->shading == SBRC_SHADE_SHELL && (p->shell_count < 1 || p->shell_count > SBRC_MAX_SHELLS))
     return SBRC_EINVAL;
@@ -530,10 +672,10 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
   if (sbrc_local_rows(p->height, p->band_rows, p->rank, p->world) == 0) return SBRC_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (p->shading) {
-    case SBRC_SHADE_NONE: launch_march1<SBRC_SHADE_NONE>(*p, s); break;
-    case SBRC_SHADE_SHADOW: launch_march1<SBRC_SHADE_SHADOW>(*p, s); break;
-    case SBRC_SHADE_SHELL: launch_march1<SBRC_SHADE_SHELL>(*p, s); break;
-    default: launch_march1<SBRC_SHADE_CONE>(*p, s); break;
+    case SBRC_SHADE_NONE: launch_march_lookup<SBRC_SHADE_NONE>(*p, s); break;
+    case SBRC_SHADE_SHADOW: launch_march_lookup<SBRC_SHADE_SHADOW>(*p, s); break;
+    case SBRC_SHADE_SHELL: launch_march_lookup<SBRC_SHADE_SHELL>(*p, s); break;
+    default: launch_march_lookup<SBRC_SHADE_CONE>(*p, s); break;
   }
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }

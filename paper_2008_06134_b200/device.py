@@ -127,24 +127,43 @@ def light_frame(cam, spec, offsets_dev: torch.Tensor | None) -> N.SbrcLightFrame
     return lf
 
 
-def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, out: torch.Tensor,
+def quad_strides(quads: torch.Tensor) -> tuple[int, int]:
+    """(layer, row) strides in float4 units of an (n, H, W, 4) texel-quad view."""
+    if (quads.dtype != torch.float32 or quads.dim() != 4 or quads.shape[3] != 4 or quads.stride(3) != 1
+            or quads.stride(2) != 4 or quads.stride(0) % 4 or quads.stride(1) % 4):
+        raise ValueError("texel quads must be an (n, H, W, 4) float32 view with packed quads along W")
+    return quads.stride(0) // 4, quads.stride(1) // 4
+
+
+def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, quads: torch.Tensor,
                  compensation_n: float, row_begin: int, row_end: int) -> N.SbrcBuildParams:
-    """``out`` is an (n, row_end-row_begin, W) float32 CUDA view with unit x stride."""
-    if out.dtype != torch.float32 or out.dim() != 3 or out.stride(2) != 1:
-        raise ValueError("build output must be an (n, rows, W) float32 view with contiguous rows")
+    """``quads`` is the (n, row_end-row_begin, W, 4) texel-quad view of the rows built."""
+    qk, qy = quad_strides(quads)
     p = N.SbrcBuildParams()
     p.volume = dvol.struct()
     p.light = light_frame(cam, spec, offsets_dev)
     p.alpha_lut = alpha_lut_dev.data_ptr()
     p.compensation_n = float(compensation_n)
     p.row_begin, p.row_end = int(row_begin), int(row_end)
-    p.layer_stride, p.row_stride = int(out.stride(0)), int(out.stride(1))
-    p.out = out.data_ptr()
+    p.quads, p.quad_layer_stride, p.quad_row_stride = quads.data_ptr(), qk, qy
     return p
 
 
+def pack_quads(plain: torch.Tensor, quads: torch.Tensor | None = None) -> torch.Tensor:
+    """Texel quads of a plain (n, H, W) float32 CUDA stack (any layer/row strides)."""
+    if plain.dtype != torch.float32 or plain.dim() != 3 or plain.stride(2) != 1:
+        raise ValueError("intensity must be an (n, H, W) float32 tensor with contiguous rows")
+    n, h, w = plain.shape
+    if quads is None:
+        quads = torch.empty((n, h, w, 4), dtype=torch.float32, device=plain.device)
+    qk, qy = quad_strides(quads)
+    N.check(N.lib.sbrc_pack_quads(plain.data_ptr(), plain.stride(0), plain.stride(1), n, h, w,
+                                  quads.data_ptr(), qk, qy, current_stream_handle()), "sbrc_pack_quads")
+    return quads
+
+
 def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_cam, buffer_spec,
-                  intensity_dev: torch.Tensor | None, light_color, voxel_size_max: float,
+                  quads_dev: torch.Tensor | None, light_color, voxel_size_max: float,
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469)."""
@@ -172,11 +191,9 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     p.et_alpha = float(settings.early_termination_alpha)
     if mode != "none":
         p.light = light_frame(buffer_cam, buffer_spec, None)
-        if intensity_dev is not None:
-            if intensity_dev.dtype != torch.float32 or intensity_dev.stride(2) != 1:
-                raise ValueError("intensity must be float32 with contiguous rows")
-            p.intensity = intensity_dev.data_ptr()
-            p.layer_stride, p.row_stride = int(intensity_dev.stride(0)), int(intensity_dev.stride(1))
+        if quads_dev is not None:
+            p.quads = quads_dev.data_ptr()
+            p.quad_layer_stride, p.quad_row_stride = quad_strides(quads_dev)
         p.light_color[:] = [float(c) for c in np.asarray(light_color, dtype=np.float64)]
         p.ambient_floor = float(settings.ambient_floor)
     if mode == "shell":

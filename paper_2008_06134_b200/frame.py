@@ -15,7 +15,7 @@ Partitioning:
   raster image on every rank.
 - Build: either replicated (every rank runs the full K1; no collective) or
   row-sharded: rank r builds light rows [r*Hs, (r+1)*Hs) into a row-major
-  [H][n][W] buffer, whose row shards are contiguous, and one all-gather
+  [H][n][W] texel-quad buffer, whose row shards are contiguous, and one all-gather
   replicates the full buffer. Texels are independent in the reference build
   (lightbuffer.py:168-198), so the sharded build needs no halo; K2 reads the
   gathered buffer through strides, so no permutation pass is needed.
@@ -106,25 +106,27 @@ class FrameRenderer:
         self.offsets = f64_tensor(spec.plane_offsets, self.dev)
         n, h, w = int(spec.n_slices), int(light_cam.resolution[1]), int(light_cam.resolution[0])
         if self.build_mode == "replicated" or self.world == 1:
-            self.storage = torch.empty((n, h, w), dtype=torch.float32, device=self.dev)
-            self.intensity = self.storage
+            self.storage = torch.empty((n, h, w, 4), dtype=torch.float32, device=self.dev)
+            self.quads = self.storage
             self.shard = None
         else:
             b, e, hs = shard_rows(h, self.world, self.rank)
-            self.storage = torch.empty((self.world * hs, n, w), dtype=torch.float32, device=self.dev)
+            # row-major [H][n][W] quads: a rank's rows are one contiguous chunk
+            self.storage = torch.empty((self.world * hs, n, w, 4), dtype=torch.float32, device=self.dev)
             self.shard_rows = (b, e)
-            self.shard = torch.empty((hs, n, w), dtype=torch.float32, device=self.dev)
-            self.intensity = self.storage[:h].permute(1, 0, 2)  # (n, H, W) view, strides (W, nW, 1)
+            self.shard = torch.empty((hs, n, w, 4), dtype=torch.float32, device=self.dev)
+            self.quads = self.storage[:h].permute(1, 0, 2, 3)  # (n, H, W, 4) view
+        self.intensity = self.quads[..., 0]
         self._render_params = None
 
     # -------------------------------------------------------------- stages
     def build(self) -> None:
         if self.shard is None:
-            build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, self.intensity, self.comp)
+            build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, self.quads, self.comp)
             return
         b, e = self.shard_rows
         if e > b:
-            view = self.shard[: e - b].permute(1, 0, 2)  # (n, rows, W) with row stride n*W
+            view = self.shard[: e - b].permute(1, 0, 2, 3)  # (n, rows, W, 4), row stride n*W quads
             build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, view, self.comp, b, e)
         all_gather_into(self.storage, self.shard, self.group)
 
@@ -133,7 +135,7 @@ class FrameRenderer:
             buf_modes = self.settings.shading_mode != "none"
             self._render_params = render_params(
                 self.dvol, self.lut, self.settings, self.cam if buf_modes else None,
-                self.spec if buf_modes else None, self.intensity if buf_modes else None,
+                self.spec if buf_modes else None, self.quads if buf_modes else None,
                 self.cam.light_color, float(self.dvol.voxel_size.max()), self.chunk, self.counter,
                 band_rows=self.band_rows, rank=self.rank, world=self.world)
         self._render_params.sample_count = self.counter.data_ptr() if count_samples else None

@@ -18,16 +18,16 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import _require_cuda, current_stream_handle, device_volume, f64_tensor, render_params
+from .device import _require_cuda, current_stream_handle, device_volume, f64_tensor, pack_quads, render_params
 from .lightbuffer import AttenuationBuffer
 from .scene import BUFFER_MODES, ConfigError
 
 
-def _intensity_of(buffer, dev) -> torch.Tensor:
+def _quads_of(buffer, dev) -> torch.Tensor:
     if isinstance(buffer, AttenuationBuffer):
-        return buffer.device_intensity(dev)
-    # a reference AttenuationBuffer (numpy intensity)
-    return torch.from_numpy(np.ascontiguousarray(buffer.intensity, dtype=np.float32)).to(dev)
+        return buffer.device_quads(dev)
+    # a reference AttenuationBuffer (numpy intensity): upload and pack
+    return pack_quads(torch.from_numpy(np.ascontiguousarray(buffer.intensity, dtype=np.float32)).to(dev))
 
 
 def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: bool = False,
@@ -53,9 +53,9 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
     counter = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
     inten, cam, spec, color = None, None, None, None
     if mode in BUFFER_MODES:
-        inten = _intensity_of(buffer, dev)
+        inten = _quads_of(buffer, dev)
         cam, spec, color = buffer.camera, buffer.spec, buffer.camera.light_color
-        n, hh, ww = inten.shape
+        n, hh, ww = inten.shape[:3]
         if (n, hh, ww) != (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0])):
             raise ValueError("attenuation intensity shape does not match its camera/stack")
     vs = float(dvol.voxel_size.max())   # ShellKernel.default(v.voxel_size.max()), :403

@@ -236,7 +236,8 @@ def test_deterministic_and_partition_invariant(sb):
 
 
 def test_sharded_layout_build_matches(sb):
-    """Row-sharded K1 into the [H][n][W] layout equals the full build."""
+    """Row-sharded K1 into the row-major [H][n][W] quad layout equals the full build,
+    and K2 reads that layout through its strides identically."""
     import torch
     from paper_2008_06134_b200.device import device_volume, f64_tensor
     from paper_2008_06134_b200.lightbuffer import build_into
@@ -247,19 +248,36 @@ def test_sharded_layout_build_matches(sb):
     n, h, w = spec.n_slices, cam.resolution[1], cam.resolution[0]
     world = 3
     hs = shard_rows(h, world, 0)[2]
-    store = torch.zeros((world * hs, n, w), dtype=torch.float32, device=dev)
+    store = torch.zeros((world * hs, n, w, 4), dtype=torch.float32, device=dev)
     alpha = f64_tensor(tf.resolve(spec.spacing)[:, 3], dev)
     offs = f64_tensor(spec.plane_offsets, dev)
     for r in range(world):
         b, e, _ = shard_rows(h, world, r)
-        build_into(device_volume(v, dev), alpha, cam, spec, offs, store[b:e].permute(1, 0, 2), 0.0, b, e)
-    inten = store[:h].permute(1, 0, 2)
-    assert np.array_equal(inten.cpu().numpy(), g["intensity"])
-    # and the march reads the strided layout identically
+        build_into(device_volume(v, dev), alpha, cam, spec, offs, store[b:e].permute(1, 0, 2, 3), 0.0, b, e)
+    quads = store[:h].permute(1, 0, 2, 3)
+    assert np.array_equal(quads[..., 0].cpu().numpy(), g["intensity"])
+    full = sb.build_attenuation_buffer(v, tf, cam, spec)
+    assert torch.equal(full.quads, quads.contiguous())
     s = settings_for("cone")
     a = sb.render(v, tf, s, sb.AttenuationBuffer(cam, spec, 0.0, g["intensity"]))
-    b = sb.render(v, tf, s, sb.AttenuationBuffer(cam, spec, 0.0, inten))
+    b = sb.render(v, tf, s, sb.AttenuationBuffer(cam, spec, 0.0, quads=quads))
     assert np.array_equal(a, b)
+
+
+def test_pack_quads_matches_build(sb):
+    """A host (reference-built) stack packed on the device equals the quads K1 writes."""
+    import torch
+    for case in ("blob32", "aniso_u16"):
+        g = load_golden(case)
+        v, tf, cam, spec, _ = scene_from_golden(g)
+        built = sb.build_attenuation_buffer(v, tf, cam, spec).quads
+        packed = sb.AttenuationBuffer(cam, spec, 0.0, g["intensity"]).device_quads()
+        assert torch.equal(built, packed)
+        q = packed.cpu().numpy()
+        I = g["intensity"]
+        assert np.array_equal(q[..., 0], I)
+        assert np.array_equal(q[:-1, :, :, 1], I[1:]) and np.array_equal(q[-1, :, :, 1], I[-1])
+        assert np.array_equal(q[:, :, :-1, 2], I[:, :, 1:]) and np.array_equal(q[:, :, -1, 2], I[:, :, -1])
 
 
 def test_u8_device_volume_is_raw(sb):
@@ -284,3 +302,23 @@ def test_frame_renderer_single_rank(sb):
     st = parity_stats(img, g["image_cone_linear"])
     assert st["max_abs"] <= TIGHT
     assert np.array_equal(fr.intensity.cpu().numpy(), g["intensity"])
+
+
+def test_single_texel_and_slice_edges(sb):
+    """Degenerate stacks: n = 1 slice, a 1-texel-wide and 1-texel-tall buffer."""
+    from oracle import slicecast_oracle as O
+    from paper_2008_06134_b200.datasets import make_sphere_blobs
+    v = make_sphere_blobs((16, 16, 16), seed=2)
+    tf = sb.preset("hot")
+    ld = (0.2, -0.3, 0.9)
+    camera = sb.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5))
+    for res, n in (((1, 1), 1), ((1, 7), 3), ((9, 1), 2), ((5, 4), 1)):
+        cam = sb.LightCamera.fit(ld, (1, 1, 1), res)
+        spec = sb.make_slice_stack(ld, n)
+        buf = sb.build_attenuation_buffer(v, tf, cam, spec)
+        assert np.array_equal(buf.intensity, O.build_intensity(v, tf.lut, cam, spec))
+        for mode, lk in (("sbrc_shadow", "linear"), ("sbrc_shadow", "nearest"), ("cone", "linear"), ("shell", "linear")):
+            s = sb.RenderSettings(camera=camera, light=sb.Light(direction=ld), viewport=(12, 10), step=1 / 40,
+                                  shading_mode=mode, lookup_mode=lk)
+            st = parity_stats(sb.render(v, tf, s, buf), O.render_image(v, tf.lut, s, buf))
+            assert st["max_abs"] <= TIGHT, (res, n, mode, lk, st)
