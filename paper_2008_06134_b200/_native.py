@@ -14,7 +14,7 @@ import os
 from .scene import ConfigError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_sbrc.so")
+LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
 ABI_VERSION = 2
 MAX_SHELLS = 8

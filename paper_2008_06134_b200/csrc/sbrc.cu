@@ -277,12 +277,31 @@ __device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float 
   return lerpf(v0, lerpf(b0, b1, fy), f);
 }
 
+// Interior tap: the caller guarantees 0 <= tx < W-1 and 0 <= ty < H-1, so the
+// footprint test passes and no clamp of light_lookup is active; the two
+// layers of quad layer offset `kbase` are accumulated separately into v0/v1
+// and blended once per layer pair by the caller.
+__device__ __forceinline__ void interior_tap(const QuadTex& t, unsigned kbase, float tx, float ty, float& v0,
+                                             float& v1) {
+  const float xl = floorf(tx), yl = floorf(ty);
+  const float fx = tx - xl, fy = ty - yl;
+  const unsigned off = kbase + (unsigned)(int)yl * t.qy + (unsigned)(int)xl;
+  const float4 r0 = __ldg(t.q + off);
+  const float4 r1 = __ldg(t.q + off + t.qy);
+  v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
+  v1 += lerpf(lerpf(r0.y, r0.w, fx), lerpf(r1.y, r1.w, fx), fy);
+}
+
 struct ShellTap {
   float dtx, dty, dli, w;  // texel-space offset of +radius along one world axis; shell weight
 };
 
+#ifndef SBRC_MARCH_MIN_BLOCKS
+#define SBRC_MARCH_MIN_BLOCKS 3  // 80 registers: 24 warps per SM (A/B in profiles/r01_notes.md)
+#endif
+
 template <int SHADING, int LOOKUP, int VT, int NSHELL, int CONE_A, int CONE_N>
-__global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) {
+__global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const sbrc_render_params P) {
   __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
@@ -297,6 +316,10 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
   const double sx = (double)LF.width / (LF.u_range[1] - LF.u_range[0]);
   const double sy = (double)LF.height / (LF.v_range[1] - LF.v_range[0]);
   const double si = (double)LF.n_slices / (LF.d_max - LF.d_min);
+  // Interior reach of the scattering kernel in texel / layer units: a sample
+  // whose light-space position is at least this far inside the buffer has all
+  // its taps inside too, and takes the clamp-free fast path.
+  float reach_x = 0.f, reach_y = 0.f, reach_l = 0.f;
   if (SHADING == SBRC_SHADE_SHELL) {
     // p +- r e_a maps to (tx, ty, li) +- r (au[a] sx, av[a] sy, L[a] si).
     for (int i = threadIdx.x; i < P.shell_count * 3; i += blockDim.x) {
@@ -305,7 +328,25 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
       shell_taps[i] = ShellTap{(float)(r * LF.axis_u[a] * sx), (float)(r * LF.axis_v[a] * sy),
                                (float)(r * LF.light_dir[a] * si), (float)P.shell_weight[s]};
     }
+    double rmax = 0.0;
+    for (int s = 0; s < P.shell_count; ++s) rmax = fmax(rmax, P.shell_radius[s]);
+    double mu = 0.0, mv = 0.0, ml = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      mu = fmax(mu, fabs(LF.axis_u[a]));
+      mv = fmax(mv, fabs(LF.axis_v[a]));
+      ml = fmax(ml, fabs(LF.light_dir[a]));
+    }
+    reach_x = (float)(rmax * mu * sx * 1.001 + 1e-3);
+    reach_y = (float)(rmax * mv * sy * 1.001 + 1e-3);
+    reach_l = (float)(rmax * ml * si * 1.001 + 1e-3);
   }
+  if (SHADING == SBRC_SHADE_CONE) {
+    const double rr = P.cone_ring * ((LF.d_max - LF.d_min) / LF.n_slices) * P.cone_axis_samples;
+    reach_x = (float)(rr * sx * 1.001 + 1e-3);
+    reach_y = (float)(rr * sy * 1.001 + 1e-3);
+  }
+  const float fast_x_hi = (float)(LF.width - 1), fast_y_hi = (float)(LF.height - 1);
+  const float fast_l_hi = (float)(LF.n_slices - 1);
   if (SHADING == SBRC_SHADE_CONE) {
     for (int i = threadIdx.x; i < P.cone_angle_count; i += blockDim.x)
       cone_cs[i] = make_float2((float)P.cone_cos[i], (float)P.cone_sin[i]);
@@ -407,6 +448,8 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
         ig = fg_c > 0.f ? 1.0f / fg_c : 0.f;
         ib = fb_c > 0.f ? 1.0f / fb_c : 0.f;
       }
+      // white light without ambient floor: factor = max(s, 0) on every channel
+      const bool white = fr_c == 1.f && fg_c == 1.f && fb_c == 1.f && P.ambient_floor == 0.f;
       // Cone ring geometry per ray (texel units): tap (i, j) sits at
       // (tx + r_i*wx_j, ty + r_i*wy_j, li - i), r_i = ring * i * spacing.
       constexpr int NA = CONE_N > 0 ? CONE_N : 1;
@@ -450,23 +493,65 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
           } else if (SHADING == SBRC_SHADE_SHELL) {
             float acc = 0.0f;
             const int nsh = NSHELL > 0 ? NSHELL : P.shell_count;
+            const bool fast = LOOKUP == SBRC_LOOKUP_LINEAR && tx - reach_x >= 0.f && tx + reach_x < fast_x_hi &&
+                              ty - reach_y >= 0.f && ty + reach_y < fast_y_hi && li - reach_l >= 0.f &&
+                              li + reach_l < fast_l_hi;
+            if (fast) {
 #pragma unroll
-            for (int sh = 0; sh < (NSHELL > 0 ? NSHELL : SBRC_MAX_SHELLS); ++sh) {
-              if (NSHELL == 0 && sh >= nsh) break;
-              float shell = 0.0f;
+              for (int sh = 0; sh < (NSHELL > 0 ? NSHELL : SBRC_MAX_SHELLS); ++sh) {
+                if (NSHELL == 0 && sh >= nsh) break;
+                float shell = 0.0f;
 #pragma unroll
-              for (int a = 0; a < 3; ++a) {
-                const ShellTap tp = shell_taps[sh * 3 + a];
-                shell += light_lookup<LOOKUP>(tex, tx + tp.dtx, ty + tp.dty, li + tp.dli);
-                shell += light_lookup<LOOKUP>(tex, tx - tp.dtx, ty - tp.dty, li - tp.dli);
+                for (int a = 0; a < 3; ++a) {
+                  const ShellTap tp = shell_taps[sh * 3 + a];
+#pragma unroll
+                  for (int sg = 0; sg < 2; ++sg) {
+                    const float sgn = sg ? -1.0f : 1.0f;
+                    const float lt = fmaf(sgn, tp.dli, li);
+                    const float kl = floorf(lt);
+                    float v0 = 0.f, v1 = 0.f;
+                    interior_tap(tex, (unsigned)(int)kl * tex.qk, fmaf(sgn, tp.dtx, tx), fmaf(sgn, tp.dty, ty), v0, v1);
+                    shell += lerpf(v0, v1, lt - kl);
+                  }
+                }
+                acc += shell_taps[sh * 3].w * shell / 6.0f;
               }
-              acc += shell_taps[sh * 3].w * shell / 6.0f;
+            } else {
+#pragma unroll
+              for (int sh = 0; sh < (NSHELL > 0 ? NSHELL : SBRC_MAX_SHELLS); ++sh) {
+                if (NSHELL == 0 && sh >= nsh) break;
+                float shell = 0.0f;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                  const ShellTap tp = shell_taps[sh * 3 + a];
+                  shell += light_lookup<LOOKUP>(tex, tx + tp.dtx, ty + tp.dty, li + tp.dli);
+                  shell += light_lookup<LOOKUP>(tex, tx - tp.dtx, ty - tp.dty, li - tp.dli);
+                }
+                acc += shell_taps[sh * 3].w * shell / 6.0f;
+              }
             }
             scalar = acc;
           } else {  // cone
             const bool degenerate = !((double)dperp * t > 1e-12);  // fallback plane_basis(L)[0] = axis_u
             float acc = 0.0f;
-            if (CONE_N > 0) {
+            const bool fast = CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR && !degenerate && tx - reach_x >= 0.f &&
+                              tx + reach_x < fast_x_hi && ty - reach_y >= 0.f && ty + reach_y < fast_y_hi &&
+                              li - (float)CONE_A >= 0.f && li - 1.0f < fast_l_hi;
+            if (fast) {
+              // every tap inside the buffer: one layer pair per ring, blended once
+#pragma unroll
+              for (int i = 1; i <= CONE_A; ++i) {
+                const float r = spacing_r * (float)i;
+                const float lt = li - (float)i;
+                const float kl = floorf(lt);
+                const unsigned kb = (unsigned)(int)kl * tex.qk;
+                float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+                for (int j = 0; j < NA; ++j) interior_tap(tex, kb, fmaf(r, wx[j], tx), fmaf(r, wy[j], ty), v0, v1);
+                acc += lerpf(v0, v1, lt - kl);
+              }
+              scalar = acc * (1.0f / (float)(CONE_A * NA));
+            } else if (CONE_N > 0) {
 #pragma unroll
               for (int i = 1; i <= CONE_A; ++i) {
                 const float r = spacing_r * (float)i;
@@ -498,9 +583,13 @@ __global__ void __launch_bounds__(256) march_kernel(const sbrc_render_params P) 
               scalar = acc / (float)(P.cone_axis_samples * P.cone_angle_count);
             }
           }
-          fr = fr_c > 0.f ? (double)(fmaxf(scalar * fr_c, P.ambient_floor) * ir) : 1.0;
-          fg = fg_c > 0.f ? (double)(fmaxf(scalar * fg_c, P.ambient_floor) * ig) : 1.0;
-          fb = fb_c > 0.f ? (double)(fmaxf(scalar * fb_c, P.ambient_floor) * ib) : 1.0;
+          if (white) {
+            fr = fg = fb = (double)fmaxf(scalar, 0.0f);
+          } else {
+            fr = fr_c > 0.f ? (double)(fmaxf(scalar * fr_c, P.ambient_floor) * ir) : 1.0;
+            fg = fg_c > 0.f ? (double)(fmaxf(scalar * fg_c, P.ambient_floor) * ig) : 1.0;
+            fb = fb_c > 0.f ? (double)(fmaxf(scalar * fb_c, P.ambient_floor) * ib) : 1.0;
+          }
         }
         // C += (1-a)*rgb*factor; a += (1-a)*a_src (raycaster.py:436-438)
         const double one_m = dsub(1.0, alpha);
