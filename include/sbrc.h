@@ -53,7 +53,8 @@ typedef enum sbrc_status {
 typedef enum sbrc_voxel_type {
   SBRC_VOXEL_F32 = 0, /* already-normalised float32 (volume.py:147-149)          */
   SBRC_VOXEL_U8 = 1,  /* raw u8, normalised at fetch as (float)x / 255.0f (volume.py:143-144) */
-  SBRC_VOXEL_U16 = 2  /* raw u16, normalised at fetch as (float)x / 65535.0f (volume.py:145-146) */
+  SBRC_VOXEL_U16 = 2, /* raw u16, normalised at fetch as (float)x / 65535.0f (volume.py:145-146) */
+  SBRC_VOXEL_F64 = 3  /* float32 values widened to float64 at upload (no per-fetch conversion) */
 } sbrc_voxel_type;
 
 typedef enum sbrc_shading {

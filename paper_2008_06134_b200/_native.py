@@ -21,7 +21,7 @@ MAX_SHELLS = 8
 MAX_ANGLES = 16
 
 OK, EINVAL, ECONFIG, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4
-VOXEL_F32, VOXEL_U8, VOXEL_U16 = 0, 1, 2
+VOXEL_F32, VOXEL_U8, VOXEL_U16, VOXEL_F64 = 0, 1, 2, 3
 SHADE = {"none": 0, "sbrc_shadow": 1, "shell": 2, "cone": 3}
 LOOKUP = {"linear": 0, "nearest": 1}
 

@@ -39,13 +39,34 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
-__device__ __forceinline__ double dclip01(double x) { return fmin(fmax(x, 0.0), 1.0); }
+__device__ __forceinline__ double dclip01(double x) { return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x); }
 __device__ __forceinline__ bool in01(double x) { return x >= 0.0 && x <= 1.0; }
+
+// Exact floors without the conversion pipe (F2I/FRND/F2F issue at a quarter
+// of the FMA rate and were a third of the march's instructions): adding
+// 1.5*2^52 (resp. 1.5*2^23) with round-toward-minus-infinity lands exactly on
+// floor(x) + magic for |x| < 2^51 (2^22); the low word is the integer.
+struct FloorD {
+  double f;
+  int i;
+};
+__device__ __forceinline__ FloorD floor_d(double x) {
+  const double m = __dadd_rd(x, 6755399441055744.0);
+  return FloorD{__dsub_rn(m, 6755399441055744.0), __double2loint(m)};
+}
+struct FloorF {
+  float f;
+  int i;
+};
+__device__ __forceinline__ FloorF floor_f(float x) {
+  const float m = __fadd_rd(x, 12582912.0f);
+  return FloorF{__fsub_rn(m, 12582912.0f), __float_as_int(m) - 0x4B400000};
+}
 
 // ---------------------------------------------------------------- volume
 // Voxel fetch with load_raw's normalisation (volume.py:143-149): u8/u16 are
 // kept raw in HBM and normalised at fetch. u8 uses a 256-entry table of
-// __fdiv_rn(x, 255.f); u16 computes (float)((double)x / 65535) through a
+// __fdiv_rn(x, 255.f) (held as double); u16 computes (float)((double)x / 65535) through a
 // double product, which rounds to the same float as the IEEE float32
 // division because x/65535 is never within 2^-40 of a float midpoint.
 // Both are bit-identical to numpy's `astype(float32) / 255.0` etc.
@@ -54,9 +75,15 @@ template <> struct Voxel<SBRC_VOXEL_F32> {
   using T = float;
   static __device__ __forceinline__ double cvt(float x, const float*) { return (double)x; }
 };
+template <> struct Voxel<SBRC_VOXEL_F64> {
+  using T = double;
+  static __device__ __forceinline__ double cvt(double x, const float*) { return x; }
+};
 template <> struct Voxel<SBRC_VOXEL_U8> {
   using T = unsigned char;
-  static __device__ __forceinline__ double cvt(unsigned char x, const float* tab) { return (double)tab[x]; }
+  static __device__ __forceinline__ double cvt(unsigned char x, const float* tab) {
+    return reinterpret_cast<const double*>(tab)[x];
+  }
 };
 template <> struct Voxel<SBRC_VOXEL_U16> {
   using T = unsigned short;
@@ -67,8 +94,10 @@ template <> struct Voxel<SBRC_VOXEL_U16> {
 
 // Cell-centred trilinear reconstruction, clamp-to-edge, 0 outside the unit
 // cube: sample_trilinear_many (volume.py:161-194), same op order. The
-// voxel index is 32-bit (validated: nx*ny*nz < 2^32).
-template <int VT>
+// voxel index is 32-bit (validated: nx*ny*nz < 2^32). UNIT: the volume box
+// is the unit cube (box_lo = 0, box_hi = 1: every cubic dataset), where
+// local = (p - 0)/1 = p exactly and the clip is a no-op inside the cube.
+template <int VT, bool UNIT>
 __device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float* u8tab, double px, double py,
                                               double pz) {
   using T = typename Voxel<VT>::T;
@@ -79,18 +108,18 @@ __device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float*
   double f[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    double local = dsub(p[c], v.box_lo[c]);
-    if (v.box_ext[c] != 1.0) local = ddiv(local, v.box_ext[c]);  // x/1.0 == x exactly
-    local = dclip01(local);
+    double local = p[c];
+    if (!UNIT) local = dclip01(ddiv(dsub(p[c], v.box_lo[c]), v.box_ext[c]));
     const double g = dsub(dmul(local, (double)dims[c]), 0.5);
-    const double fl = floor(g);
-    f[c] = dsub(g, fl);
-    lo[c] = (int)fl;
+    const FloorD fl = floor_d(g);
+    f[c] = dsub(g, fl.f);
+    lo[c] = fl.i;
   }
   const T* base = reinterpret_cast<const T*>(v.data);
   const unsigned nx = (unsigned)v.nx, nxy = (unsigned)v.nx * (unsigned)v.ny;
   T r000, r100, r010, r110, r001, r101, r011, r111;
-  if (lo[0] >= 0 && lo[0] < v.nx - 1 && lo[1] >= 0 && lo[1] < v.ny - 1 && lo[2] >= 0 && lo[2] < v.nz - 1) {
+  if ((unsigned)lo[0] < (unsigned)(v.nx - 1) && (unsigned)lo[1] < (unsigned)(v.ny - 1) &&
+      (unsigned)lo[2] < (unsigned)(v.nz - 1)) {
     // interior: the 2x2x2 cell without clamping
     const T* c = base + ((unsigned)lo[0] + nx * (unsigned)lo[1] + nxy * (unsigned)lo[2]);
     const T* cy = c + nx;
@@ -123,10 +152,10 @@ __device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float*
   return dadd(dmul(c0, gz), dmul(c1, f[2]));
 }
 
-// u8 normalisation table: tab[x] = (float)x / 255.0f, IEEE division.
-__device__ __forceinline__ void fill_u8_table(float* tab) {
+// u8 normalisation table: tab[x] = (double)((float)x / 255.0f), IEEE division.
+__device__ __forceinline__ void fill_u8_table(double* tab) {
   for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < 256; i += blockDim.x * blockDim.y)
-    tab[i] = __fdiv_rn((float)i, 255.0f);
+    tab[i] = (double)__fdiv_rn((float)i, 255.0f);
 }
 
 // LUT position: t = clip(s,0,1)*255, i0 = floor(t) (truncation, s >= 0),
@@ -138,10 +167,10 @@ struct LutPos {
 __device__ __forceinline__ LutPos lut_pos(double s) {
   LutPos r;
   const double t = dmul(dclip01(s), 255.0);
-  const double fl = floor(t);
-  r.i0 = (int)fl;
+  const FloorD fl = floor_d(t);
+  r.i0 = fl.i;
   r.i1 = min(r.i0 + 1, SBRC_LUT_SIZE - 1);
-  r.f = dsub(t, fl);
+  r.f = dsub(t, fl.f);
   r.g = dsub(1.0, r.f);
   return r;
 }
@@ -163,10 +192,10 @@ __device__ __forceinline__ void emit_pair(float4* row, int x, int w, float a, fl
 // the cube, alpha = lut(trilinear(p)) and T *= 1 - alpha. Texels are
 // independent, so no grid-wide barrier or per-slice launch is needed. The
 // quad of layer k needs layer k+1, so it is emitted one slice late.
-template <int VT>
+template <int VT, bool UNIT>
 __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   __shared__ double lut[SBRC_LUT_SIZE];
-  __shared__ float u8tab[256];
+  __shared__ double u8tab[256];
   for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x * blockDim.y)
     lut[i] = P.alpha_lut[i];
   if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
@@ -201,7 +230,7 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
     const double pz = dadd(base[2], dmul(off, L.light_dir[2]));
     float stored = (float)T;  // intensity[k] = trans (:169)
     if (in01(px) && in01(py) && in01(pz)) {
-      const double s = trilinear64<VT>(P.volume, u8tab, px, py, pz);
+      const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), px, py, pz);
       const LutPos q = lut_pos(s);
       const double a = dadd(dmul(lut[q.i0], q.g), dmul(lut[q.i1], q.f));
       if (comp) stored = (float)dmul((double)stored, pow(dadd(1.0, a), P.compensation_n));  // :193-196
@@ -254,17 +283,17 @@ template <int LOOKUP>
 __device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float ty, float li_raw) {
   // li_raw: idx - 0.5 for linear lookups, idx for nearest
   if (!(tx >= -0.5f && tx <= t.txmax && ty >= -0.5f && ty <= t.tymax)) return 1.0f;
-  const float xa = fminf(fmaxf(floorf(tx), 0.0f), t.xa_max);
-  const float ya = fminf(fmaxf(floorf(ty), 0.0f), t.ya_max);
+  const float xa = fminf(fmaxf(floor_f(tx).f, 0.0f), t.xa_max);
+  const float ya = fminf(fmaxf(floor_f(ty).f, 0.0f), t.ya_max);
   const float fx = __saturatef(tx - xa), fy = __saturatef(ty - ya);
   float ka, f;
   if (LOOKUP == SBRC_LOOKUP_NEAREST) {
     // k = floor(clip(idx, 0, n-1)) (:275); for nearest lookups li_raw is idx
-    ka = floorf(fminf(fmaxf(li_raw, 0.0f), t.li_max));
+    ka = floor_f(fminf(fmaxf(li_raw, 0.0f), t.li_max)).f;
     f = 0.0f;
   } else {
     const float li = fminf(fmaxf(li_raw, 0.0f), t.li_max);
-    ka = fminf(floorf(li), t.ka_max);
+    ka = fminf(floor_f(li).f, t.ka_max);
     f = li - ka;
   }
   const unsigned off = (unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa;
@@ -283,9 +312,9 @@ __device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float 
 // and blended once per layer pair by the caller.
 __device__ __forceinline__ void interior_tap(const QuadTex& t, unsigned kbase, float tx, float ty, float& v0,
                                              float& v1) {
-  const float xl = floorf(tx), yl = floorf(ty);
-  const float fx = tx - xl, fy = ty - yl;
-  const unsigned off = kbase + (unsigned)(int)yl * t.qy + (unsigned)(int)xl;
+  const FloorF xl = floor_f(tx), yl = floor_f(ty);
+  const float fx = tx - xl.f, fy = ty - yl.f;
+  const unsigned off = kbase + (unsigned)yl.i * t.qy + (unsigned)xl.i;
   const float4 r0 = __ldg(t.q + off);
   const float4 r1 = __ldg(t.q + off + t.qy);
   v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
@@ -300,12 +329,12 @@ struct ShellTap {
 #define SBRC_MARCH_MIN_BLOCKS 3  // 80 registers: 24 warps per SM (A/B in profiles/r01_notes.md)
 #endif
 
-template <int SHADING, int LOOKUP, int VT, int NSHELL, int CONE_A, int CONE_N>
+template <int SHADING, int LOOKUP, int VT, bool UNIT, int NSHELL, int CONE_A, int CONE_N>
 __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const sbrc_render_params P) {
   __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
-  __shared__ float u8tab[256];
+  __shared__ double u8tab[256];
   for (int i = threadIdx.x; i < SBRC_LUT_SIZE * 2; i += blockDim.x)
     lut[i] = reinterpret_cast<const double2*>(P.lut_rgba)[i];
   if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
@@ -466,6 +495,12 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
       }
       const double step = P.step, thresh = P.et_alpha;
       double t = dadd(t_enter, 0.5 * step);
+      // fp32 light-space centre: c(t) ~= c(t0) + j * step * dc/dt with a float
+      // sample counter j (exact below 2^24), so no conversion per sample; the
+      // float64 t stays the sample-position authority.
+      const float ftx0 = (float)fma(t, txd, tx0), fty0 = (float)fma(t, tyd, ty0), fli0 = (float)fma(t, lid, li0);
+      const float ftxs = (float)(txd * step), ftys = (float)(tyd * step), flis = (float)(lid * step);
+      float jf = 0.0f;
       double cr = 0.0, cg = 0.0, cb = 0.0, alpha = 0.0;
       // Front-to-back march (raycaster.py:428-439): the live test precedes
       // each sample, so the sample that crosses the threshold is kept.
@@ -473,7 +508,7 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
         const double qx = dadd(P.eye[0], dmul(t, d[0]));
         const double qy = dadd(P.eye[1], dmul(t, d[1]));
         const double qz = dadd(P.eye[2], dmul(t, d[2]));
-        const double s = trilinear64<VT>(P.volume, u8tab, qx, qy, qz);
+        const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), qx, qy, qz);
         const LutPos q = lut_pos(s);
         const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
         const double2 b_rg = lut[2 * q.i1], b_ba = lut[2 * q.i1 + 1];
@@ -484,9 +519,9 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
 
         double fr = 1.0, fg = 1.0, fb = 1.0;
         if (SHADING != SBRC_SHADE_NONE) {
-          const float tx = (float)fma(t, txd, tx0);
-          const float ty = (float)fma(t, tyd, ty0);
-          const float li = (float)fma(t, lid, li0);
+          const float tx = fmaf(jf, ftxs, ftx0);
+          const float ty = fmaf(jf, ftys, fty0);
+          const float li = fmaf(jf, flis, fli0);
           float scalar;
           if (SHADING == SBRC_SHADE_SHADOW) {
             scalar = light_lookup<LOOKUP>(tex, tx, ty, li);
@@ -508,10 +543,10 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
                   for (int sg = 0; sg < 2; ++sg) {
                     const float sgn = sg ? -1.0f : 1.0f;
                     const float lt = fmaf(sgn, tp.dli, li);
-                    const float kl = floorf(lt);
+                    const FloorF kl = floor_f(lt);
                     float v0 = 0.f, v1 = 0.f;
-                    interior_tap(tex, (unsigned)(int)kl * tex.qk, fmaf(sgn, tp.dtx, tx), fmaf(sgn, tp.dty, ty), v0, v1);
-                    shell += lerpf(v0, v1, lt - kl);
+                    interior_tap(tex, (unsigned)kl.i * tex.qk, fmaf(sgn, tp.dtx, tx), fmaf(sgn, tp.dty, ty), v0, v1);
+                    shell += lerpf(v0, v1, lt - kl.f);
                   }
                 }
                 acc += shell_taps[sh * 3].w * shell / 6.0f;
@@ -543,12 +578,12 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
               for (int i = 1; i <= CONE_A; ++i) {
                 const float r = spacing_r * (float)i;
                 const float lt = li - (float)i;
-                const float kl = floorf(lt);
-                const unsigned kb = (unsigned)(int)kl * tex.qk;
+                const FloorF kl = floor_f(lt);
+                const unsigned kb = (unsigned)kl.i * tex.qk;
                 float v0 = 0.f, v1 = 0.f;
 #pragma unroll
                 for (int j = 0; j < NA; ++j) interior_tap(tex, kb, fmaf(r, wx[j], tx), fmaf(r, wy[j], ty), v0, v1);
-                acc += lerpf(v0, v1, lt - kl);
+                acc += lerpf(v0, v1, lt - kl.f);
               }
               scalar = acc * (1.0f / (float)(CONE_A * NA));
             } else if (CONE_N > 0) {
@@ -598,6 +633,7 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
         cb = dadd(cb, dmul(dmul(one_m, sb), fb));
         alpha = dadd(alpha, dmul(one_m, sa));
         t = dadd(t, step);
+        jf += 1.0f;
         ++samples;
       }
       result = make_float4((float)cr, (float)cg, (float)cb, (float)alpha);
@@ -616,7 +652,7 @@ bool volume_ok(const sbrc_volume& v) {
   if (v.data == nullptr) return false;
   if (v.nx < 2 || v.ny < 2 || v.nz < 2) return false;  // volume.py:80-81
   if ((unsigned long long)v.nx * v.ny * v.nz >= (1ull << 32)) return false;  // 32-bit voxel offsets
-  if (v.voxel_type < SBRC_VOXEL_F32 || v.voxel_type > SBRC_VOXEL_U16) return false;
+  if (v.voxel_type < SBRC_VOXEL_F32 || v.voxel_type > SBRC_VOXEL_F64) return false;
   for (int c = 0; c < 3; ++c)
     if (!(v.box_ext[c] > 0.0)) return false;
   return true;
@@ -634,38 +670,51 @@ bool quads_ok(const sbrc_light_frame& L, int64_t qk, int64_t qy) {
   return last < (1ll << 32);
 }
 
+bool unit_box(const sbrc_volume& v) {
+  for (int c = 0; c < 3; ++c)
+    if (v.box_lo[c] != 0.0 || v.box_ext[c] != 1.0) return false;
+  return true;
+}
+
 template <int VT>
 void launch_build(const sbrc_build_params& p, cudaStream_t s) {
   dim3 block(32, 8);
   dim3 grid((p.light.width + 31) / 32, (p.row_end - p.row_begin + 7) / 8);
-  build_kernel<VT><<<grid, block, 0, s>>>(p);
+  if (unit_box(p.volume)) build_kernel<VT, true><<<grid, block, 0, s>>>(p);
+  else build_kernel<VT, false><<<grid, block, 0, s>>>(p);
 }
 
-template <int SH, int LK, int VT, int NS, int CA, int CN>
+template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN>
 void launch_march(const sbrc_render_params& p, cudaStream_t s) {
   const int rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
   dim3 grid((p.width + 31) / 32, (rows + 7) / 8);
-  march_kernel<SH, LK, VT, NS, CA, CN><<<grid, 256, 0, s>>>(p);
+  march_kernel<SH, LK, VT, UNIT, NS, CA, CN><<<grid, 256, 0, s>>>(p);
 }
 
-template <int SH, int LK, int VT>
+template <int SH, int LK, int VT, bool UNIT>
 void launch_march_kernel_shape(const sbrc_render_params& p, cudaStream_t s) {
   if (SH == SBRC_SHADE_SHELL) {
-    if (p.shell_count == 3) launch_march<SH, LK, VT, 3, 0, 0>(p, s);
-    else launch_march<SH, LK, VT, 0, 0, 0>(p, s);
+    if (p.shell_count == 3) launch_march<SH, LK, VT, UNIT, 3, 0, 0>(p, s);
+    else launch_march<SH, LK, VT, UNIT, 0, 0, 0>(p, s);
   } else if (SH == SBRC_SHADE_CONE) {
-    if (p.cone_axis_samples == 2 && p.cone_angle_count == 4) launch_march<SH, LK, VT, 0, 2, 4>(p, s);
-    else launch_march<SH, LK, VT, 0, 0, 0>(p, s);
+    if (p.cone_axis_samples == 2 && p.cone_angle_count == 4) launch_march<SH, LK, VT, UNIT, 0, 2, 4>(p, s);
+    else launch_march<SH, LK, VT, UNIT, 0, 0, 0>(p, s);
   } else {
-    launch_march<SH, LK, VT, 0, 0, 0>(p, s);
+    launch_march<SH, LK, VT, UNIT, 0, 0, 0>(p, s);
   }
+}
+template <int SH, int LK, int VT>
+void launch_march_box(const sbrc_render_params& p, cudaStream_t s) {
+  if (unit_box(p.volume)) launch_march_kernel_shape<SH, LK, VT, true>(p, s);
+  else launch_march_kernel_shape<SH, LK, VT, false>(p, s);
 }
 template <int SH, int LK>
 void launch_march_vt(const sbrc_render_params& p, cudaStream_t s) {
   switch (p.volume.voxel_type) {
-    case SBRC_VOXEL_F32: launch_march_kernel_shape<SH, LK, SBRC_VOXEL_F32>(p, s); break;
-    case SBRC_VOXEL_U8: launch_march_kernel_shape<SH, LK, SBRC_VOXEL_U8>(p, s); break;
-    default: launch_march_kernel_shape<SH, LK, SBRC_VOXEL_U16>(p, s); break;
+    case SBRC_VOXEL_F32: launch_march_box<SH, LK, SBRC_VOXEL_F32>(p, s); break;
+    case SBRC_VOXEL_F64: launch_march_box<SH, LK, SBRC_VOXEL_F64>(p, s); break;
+    case SBRC_VOXEL_U8: launch_march_box<SH, LK, SBRC_VOXEL_U8>(p, s); break;
+    default: launch_march_box<SH, LK, SBRC_VOXEL_U16>(p, s); break;
   }
 }
 template <int SH>
@@ -719,6 +768,7 @@ int sbrc_build(const sbrc_build_params* p, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (p->volume.voxel_type) {
     case SBRC_VOXEL_F32: launch_build<SBRC_VOXEL_F32>(*p, s); break;
+    case SBRC_VOXEL_F64: launch_build<SBRC_VOXEL_F64>(*p, s); break;
     case SBRC_VOXEL_U8: launch_build<SBRC_VOXEL_U8>(*p, s); break;
     default: launch_build<SBRC_VOXEL_U16>(*p, s); break;
   }

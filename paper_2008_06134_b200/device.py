@@ -46,6 +46,13 @@ class DeviceVolume:
         """(box_hi - box_lo) / dims, as VolumeDataset.voxel_size (volume.py:119-122)."""
         return (self.box_hi - self.box_lo) / np.array(self.dims, dtype=np.float64)
 
+    def widened(self) -> "DeviceVolume":
+        """A float64 copy of a float32 volume (SBRC_VOXEL_F64): the trilinear
+        fetch then needs no f32->f64 conversion per voxel (same values)."""
+        if self.voxel_type != N.VOXEL_F32:
+            raise ValueError("only float32 volumes are widened")
+        return DeviceVolume(self.data.double(), N.VOXEL_F64, self.dims, self.box_lo, self.box_hi)
+
     @property
     def nbytes(self) -> int:
         return self.data.numel() * self.data.element_size()

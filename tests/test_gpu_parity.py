@@ -322,3 +322,38 @@ def test_single_texel_and_slice_edges(sb):
                                   shading_mode=mode, lookup_mode=lk)
             st = parity_stats(sb.render(v, tf, s, buf), O.render_image(v, tf.lut, s, buf))
             assert st["max_abs"] <= TIGHT, (res, n, mode, lk, st)
+
+
+def test_widened_volume_identical(sb):
+    """A float64 device copy of a float32 volume gives bit-identical results."""
+    from paper_2008_06134_b200.device import DeviceVolume
+    g = load_golden("blob32")
+    v, tf, cam, spec, settings_for = scene_from_golden(g)
+    dv = DeviceVolume.from_dataset(v)
+    wide = dv.widened()
+    a = sb.build_attenuation_buffer(dv, tf, cam, spec)
+    b = sb.build_attenuation_buffer(wide, tf, cam, spec)
+    assert np.array_equal(a.intensity, b.intensity)
+    for mode in ("none", "cone", "shell"):
+        s = settings_for(mode)
+        assert np.array_equal(sb.render(dv, tf, s, a if mode != "none" else None),
+                              sb.render(wide, tf, s, b if mode != "none" else None))
+
+
+def test_anisotropic_box_general_path(sb):
+    """Non-unit volume box (anisotropic spacing) takes the exact-division trilinear path."""
+    from oracle import slicecast_oracle as O
+    from paper_2008_06134_b200.datasets import make_sphere_blobs
+    base = make_sphere_blobs((20, 26, 14), seed=4)
+    v = sb.VolumeDataset.from_array(base.data, spacing=(1.3, 1.0, 0.8))
+    tf = sb.preset("hot")
+    ld = (0.5, 0.4, -0.77)
+    cam = sb.LightCamera.fit(ld, (1, 1, 1), (30, 26))
+    spec = sb.make_slice_stack(ld, 20)
+    buf = sb.build_attenuation_buffer(v, tf, cam, spec)
+    assert np.array_equal(buf.intensity, O.build_intensity(v, tf.lut, cam, spec))
+    s = sb.RenderSettings(camera=sb.Camera(position=(1.6, -0.9, 1.8), target=(0.5, 0.5, 0.5)),
+                          light=sb.Light(direction=ld), viewport=(34, 30), step=1 / 50, shading_mode="cone")
+    assert parity_stats(sb.render(v, tf, s, buf), O.render_image(v, tf.lut, s, buf))["max_abs"] <= TIGHT
+    s0 = sb.RenderSettings(camera=s.camera, light=s.light, viewport=(34, 30), step=1 / 50)
+    assert np.array_equal(sb.render(v, tf, s0), O.render_image(v, tf.lut, s0))
