@@ -93,31 +93,36 @@ template <> struct Voxel<SBRC_VOXEL_U16> {
 };
 
 // Cell-centred trilinear reconstruction, clamp-to-edge, 0 outside the unit
-// cube: sample_trilinear_many (volume.py:161-194), same op order. The
-// voxel index is 32-bit (validated: nx*ny*nz < 2^32). UNIT: the volume box
-// is the unit cube (box_lo = 0, box_hi = 1: every cubic dataset), where
-// local = (p - 0)/1 = p exactly and the clip is a no-op inside the cube.
+// cube: sample_trilinear_many (volume.py:161-194), same op order. Split in
+// cell_fetch (indices, fractions, the 8 gathers) and cell_combine (the
+// float64 lerps) so callers can issue the gathers of the next slice/sample
+// before combining the current one. The voxel index is 32-bit (validated:
+// nx*ny*nz < 2^32). UNIT: the volume box is the unit cube (box_lo = 0,
+// box_hi = 1: every cubic dataset), where local = (p - 0)/1 = p exactly and
+// the clip is a no-op inside the cube.
+template <int VT>
+struct Cell {
+  typename Voxel<VT>::T r[8];  // d000 d100 d010 d110 d001 d101 d011 d111
+  double f[3];
+};
+
 template <int VT, bool UNIT>
-__device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float* u8tab, double px, double py,
-                                              double pz) {
+__device__ __forceinline__ void cell_fetch(const sbrc_volume& v, double px, double py, double pz, Cell<VT>& cl) {
   using T = typename Voxel<VT>::T;
-  if (!(in01(px) && in01(py) && in01(pz))) return 0.0;
   const double p[3] = {px, py, pz};
   const int dims[3] = {v.nx, v.ny, v.nz};
   int lo[3];
-  double f[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     double local = p[c];
     if (!UNIT) local = dclip01(ddiv(dsub(p[c], v.box_lo[c]), v.box_ext[c]));
     const double g = dsub(dmul(local, (double)dims[c]), 0.5);
     const FloorD fl = floor_d(g);
-    f[c] = dsub(g, fl.f);
+    cl.f[c] = dsub(g, fl.f);
     lo[c] = fl.i;
   }
   const T* base = reinterpret_cast<const T*>(v.data);
   const unsigned nx = (unsigned)v.nx, nxy = (unsigned)v.nx * (unsigned)v.ny;
-  T r000, r100, r010, r110, r001, r101, r011, r111;
   if ((unsigned)lo[0] < (unsigned)(v.nx - 1) && (unsigned)lo[1] < (unsigned)(v.ny - 1) &&
       (unsigned)lo[2] < (unsigned)(v.nz - 1)) {
     // interior: the 2x2x2 cell without clamping
@@ -125,8 +130,8 @@ __device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float*
     const T* cy = c + nx;
     const T* cz = c + nxy;
     const T* cyz = cz + nx;
-    r000 = __ldg(c); r100 = __ldg(c + 1); r010 = __ldg(cy); r110 = __ldg(cy + 1);
-    r001 = __ldg(cz); r101 = __ldg(cz + 1); r011 = __ldg(cyz); r111 = __ldg(cyz + 1);
+    cl.r[0] = __ldg(c); cl.r[1] = __ldg(c + 1); cl.r[2] = __ldg(cy); cl.r[3] = __ldg(cy + 1);
+    cl.r[4] = __ldg(cz); cl.r[5] = __ldg(cz + 1); cl.r[6] = __ldg(cyz); cl.r[7] = __ldg(cyz + 1);
   } else {
     // faces: i0 = clip(lo), i1 = clip(lo + 1) (volume.py:180-182)
     unsigned a[3], b[3];
@@ -136,20 +141,36 @@ __device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float*
       b[c] = (unsigned)min(max(lo[c] + 1, 0), dims[c] - 1);
     }
     const unsigned z0 = a[2] * nxy, z1 = b[2] * nxy, y0 = a[1] * nx, y1 = b[1] * nx;
-    r000 = __ldg(base + (z0 + y0 + a[0])); r100 = __ldg(base + (z0 + y0 + b[0]));
-    r010 = __ldg(base + (z0 + y1 + a[0])); r110 = __ldg(base + (z0 + y1 + b[0]));
-    r001 = __ldg(base + (z1 + y0 + a[0])); r101 = __ldg(base + (z1 + y0 + b[0]));
-    r011 = __ldg(base + (z1 + y1 + a[0])); r111 = __ldg(base + (z1 + y1 + b[0]));
+    cl.r[0] = __ldg(base + (z0 + y0 + a[0])); cl.r[1] = __ldg(base + (z0 + y0 + b[0]));
+    cl.r[2] = __ldg(base + (z0 + y1 + a[0])); cl.r[3] = __ldg(base + (z0 + y1 + b[0]));
+    cl.r[4] = __ldg(base + (z1 + y0 + a[0])); cl.r[5] = __ldg(base + (z1 + y0 + b[0]));
+    cl.r[6] = __ldg(base + (z1 + y1 + a[0])); cl.r[7] = __ldg(base + (z1 + y1 + b[0]));
   }
+}
+
+template <int VT>
+__device__ __forceinline__ double cell_combine(const Cell<VT>& cl, const float* u8tab) {
   using V = Voxel<VT>;
+  const double* f = cl.f;
   const double gx = dsub(1.0, f[0]), gy = dsub(1.0, f[1]), gz = dsub(1.0, f[2]);
-  const double c00 = dadd(dmul(V::cvt(r000, u8tab), gx), dmul(V::cvt(r100, u8tab), f[0]));
-  const double c10 = dadd(dmul(V::cvt(r010, u8tab), gx), dmul(V::cvt(r110, u8tab), f[0]));
-  const double c01 = dadd(dmul(V::cvt(r001, u8tab), gx), dmul(V::cvt(r101, u8tab), f[0]));
-  const double c11 = dadd(dmul(V::cvt(r011, u8tab), gx), dmul(V::cvt(r111, u8tab), f[0]));
+  const double c00 = dadd(dmul(V::cvt(cl.r[0], u8tab), gx), dmul(V::cvt(cl.r[1], u8tab), f[0]));
+  const double c10 = dadd(dmul(V::cvt(cl.r[2], u8tab), gx), dmul(V::cvt(cl.r[3], u8tab), f[0]));
+  const double c01 = dadd(dmul(V::cvt(cl.r[4], u8tab), gx), dmul(V::cvt(cl.r[5], u8tab), f[0]));
+  const double c11 = dadd(dmul(V::cvt(cl.r[6], u8tab), gx), dmul(V::cvt(cl.r[7], u8tab), f[0]));
   const double c0 = dadd(dmul(c00, gy), dmul(c10, f[1]));
   const double c1 = dadd(dmul(c01, gy), dmul(c11, f[1]));
   return dadd(dmul(c0, gz), dmul(c1, f[2]));
+}
+
+__device__ __forceinline__ bool in_cube(double px, double py, double pz) { return in01(px) && in01(py) && in01(pz); }
+
+template <int VT, bool UNIT>
+__device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float* u8tab, double px, double py,
+                                              double pz) {
+  if (!in_cube(px, py, pz)) return 0.0;
+  Cell<VT> cl;
+  cell_fetch<VT, UNIT>(v, px, py, pz, cl);
+  return cell_combine<VT>(cl, u8tab);
 }
 
 // u8 normalisation table: tab[x] = (double)((float)x / 255.0f), IEEE division.
@@ -220,24 +241,54 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   const bool comp = P.compensation_n > 0.0;
   float4* row = reinterpret_cast<float4*>(P.quads) + (size_t)(y - P.row_begin) * (size_t)P.quad_row_stride;
   const size_t ks = (size_t)P.quad_layer_stride;
+  const float* tab = reinterpret_cast<const float*>(u8tab);
   double T = 1.0;
   float prev = 0.0f;
-  for (int k = 0; k < L.n_slices; ++k) {
-    const double off = __ldg(L.plane_offsets + k);
-    // pts = base + offset_k * L (:182); covered = all(0 <= pts <= 1) (:183)
-    const double px = dadd(base[0], dmul(off, L.light_dir[0]));
-    const double py = dadd(base[1], dmul(off, L.light_dir[1]));
-    const double pz = dadd(base[2], dmul(off, L.light_dir[2]));
-    float stored = (float)T;  // intensity[k] = trans (:169)
-    if (in01(px) && in01(py) && in01(pz)) {
-      const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), px, py, pz);
-      const LutPos q = lut_pos(s);
+  // One slice of the recurrence: stored = T (:169); if covered, alpha from the
+  // cell, optional compensation (:193-196), T *= 1 - alpha (:197-198).
+  auto step_slice = [&](bool covered, const Cell<VT>& cl) -> float {
+    float stored = (float)T;
+    if (covered) {
+      const LutPos q = lut_pos(cell_combine<VT>(cl, tab));
       const double a = dadd(dmul(lut[q.i0], q.g), dmul(lut[q.i1], q.f));
-      if (comp) stored = (float)dmul((double)stored, pow(dadd(1.0, a), P.compensation_n));  // :193-196
-      T = dmul(T, dsub(1.0, a));  // :197-198
+      if (comp) stored = (float)dmul((double)stored, pow(dadd(1.0, a), P.compensation_n));
+      T = dmul(T, dsub(1.0, a));
     }
-    if (k > 0) emit_pair(row + (size_t)(k - 1) * ks, x, L.width, prev, stored);
-    prev = stored;
+    return stored;
+  };
+  // pts = base + offset_k * L (:182); covered = all(0 <= pts <= 1) (:183)
+  auto point = [&](int k, double& px, double& py, double& pz) {
+    const double off = __ldg(L.plane_offsets + k);
+    px = dadd(base[0], dmul(off, L.light_dir[0]));
+    py = dadd(base[1], dmul(off, L.light_dir[1]));
+    pz = dadd(base[2], dmul(off, L.light_dir[2]));
+  };
+  int k = 0;
+  // Slices in pairs: the gathers of both are issued before either is combined
+  // (the product order of T is unchanged, so the result stays bit-exact).
+  for (; k + 1 < L.n_slices; k += 2) {
+    double ax, ay, az, bx, by, bz;
+    point(k, ax, ay, az);
+    point(k + 1, bx, by, bz);
+    const bool ca = in_cube(ax, ay, az), cb = in_cube(bx, by, bz);
+    Cell<VT> la, lb;
+    if (ca) cell_fetch<VT, UNIT>(P.volume, ax, ay, az, la);
+    if (cb) cell_fetch<VT, UNIT>(P.volume, bx, by, bz, lb);
+    const float sa = step_slice(ca, la);
+    const float sb = step_slice(cb, lb);
+    if (k > 0) emit_pair(row + (size_t)(k - 1) * ks, x, L.width, prev, sa);
+    emit_pair(row + (size_t)k * ks, x, L.width, sa, sb);
+    prev = sb;
+  }
+  if (k < L.n_slices) {
+    double ax, ay, az;
+    point(k, ax, ay, az);
+    const bool ca = in_cube(ax, ay, az);
+    Cell<VT> la;
+    if (ca) cell_fetch<VT, UNIT>(P.volume, ax, ay, az, la);
+    const float sa = step_slice(ca, la);
+    if (k > 0) emit_pair(row + (size_t)(k - 1) * ks, x, L.width, prev, sa);
+    prev = sa;
   }
   emit_pair(row + (size_t)(L.n_slices - 1) * ks, x, L.width, prev, prev);
 }
@@ -325,8 +376,11 @@ struct ShellTap {
   float dtx, dty, dli, w;  // texel-space offset of +radius along one world axis; shell weight
 };
 
+#ifndef SBRC_MARCH_PREFETCH
+#define SBRC_MARCH_PREFETCH 1
+#endif
 #ifndef SBRC_MARCH_MIN_BLOCKS
-#define SBRC_MARCH_MIN_BLOCKS 3  // 80 registers: 24 warps per SM (A/B in profiles/r01_notes.md)
+#define SBRC_MARCH_MIN_BLOCKS 2  // 128 registers, no spills: 16 warps per SM (A/B in profiles/r01_notes.md)
 #endif
 
 template <int SHADING, int LOOKUP, int VT, bool UNIT, int NSHELL, int CONE_A, int CONE_N>
@@ -504,11 +558,38 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
       double cr = 0.0, cg = 0.0, cb = 0.0, alpha = 0.0;
       // Front-to-back march (raycaster.py:428-439): the live test precedes
       // each sample, so the sample that crosses the threshold is kept.
+#if SBRC_MARCH_PREFETCH
+      // the voxel cell of sample j+1 is gathered while sample j is shaded
+      // (harmless past the exit: outside the cube nothing is fetched)
+      Cell<VT> cur;
+      bool cur_in;
+      {
+        const double qx = dadd(P.eye[0], dmul(t, d[0]));
+        const double qy = dadd(P.eye[1], dmul(t, d[1]));
+        const double qz = dadd(P.eye[2], dmul(t, d[2]));
+        cur_in = in_cube(qx, qy, qz);
+        if (cur_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, cur);
+      }
+#endif
       while (t < t_far && alpha < thresh) {
+#if SBRC_MARCH_PREFETCH
+        const double tn = dadd(t, step);
+        Cell<VT> nxt;
+        bool nxt_in;
+        {
+          const double qx = dadd(P.eye[0], dmul(tn, d[0]));
+          const double qy = dadd(P.eye[1], dmul(tn, d[1]));
+          const double qz = dadd(P.eye[2], dmul(tn, d[2]));
+          nxt_in = in_cube(qx, qy, qz);
+          if (nxt_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, nxt);
+        }
+        const double s = cur_in ? cell_combine<VT>(cur, reinterpret_cast<const float*>(u8tab)) : 0.0;
+#else
         const double qx = dadd(P.eye[0], dmul(t, d[0]));
         const double qy = dadd(P.eye[1], dmul(t, d[1]));
         const double qz = dadd(P.eye[2], dmul(t, d[2]));
         const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), qx, qy, qz);
+#endif
         const LutPos q = lut_pos(s);
         const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
         const double2 b_rg = lut[2 * q.i1], b_ba = lut[2 * q.i1 + 1];
@@ -632,7 +713,13 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
         cg = dadd(cg, dmul(dmul(one_m, sg), fg));
         cb = dadd(cb, dmul(dmul(one_m, sb), fb));
         alpha = dadd(alpha, dmul(one_m, sa));
+#if SBRC_MARCH_PREFETCH
+        t = tn;
+        cur = nxt;
+        cur_in = nxt_in;
+#else
         t = dadd(t, step);
+#endif
         jf += 1.0f;
         ++samples;
       }

@@ -1,5 +1,5 @@
 import json, sys
-lab = None
+lab = "(run)"
 for l in open(sys.argv[1]):
     if l.startswith('=='):
         lab = l.strip()
