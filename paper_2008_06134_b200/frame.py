@@ -98,6 +98,22 @@ class FrameRenderer:
         self.set_light(light_cam, spec)
 
     # -------------------------------------------------------------- light
+    def prepare_light(self, light_cam, spec):
+        """Device copies of a light frame's small inputs (alpha LUT at the slice
+        spacing, plane offsets), so a moving light costs no allocation per frame."""
+        check_frame(light_cam, spec)
+        return (light_cam, spec, f64_tensor(self.tf.resolve(spec.spacing)[:, 3], self.dev),
+                f64_tensor(spec.plane_offsets, self.dev))
+
+    def use_light(self, prepared) -> None:
+        """Switch to a prepared light frame; the buffer is reused when its shape is unchanged."""
+        cam, spec, alpha, offsets = prepared
+        shape = (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0]))
+        if getattr(self, "_shape", None) != shape:
+            self.set_light(cam, spec)
+        self.cam, self.spec, self.alpha, self.offsets = cam, spec, alpha, offsets
+        self._render_params = None
+
     def set_light(self, light_cam, spec) -> None:
         """(Re)allocate the attenuation buffer for a light frame (config 5 moves the light)."""
         check_frame(light_cam, spec)
@@ -105,6 +121,7 @@ class FrameRenderer:
         self.alpha = f64_tensor(self.tf.resolve(spec.spacing)[:, 3], self.dev)
         self.offsets = f64_tensor(spec.plane_offsets, self.dev)
         n, h, w = int(spec.n_slices), int(light_cam.resolution[1]), int(light_cam.resolution[0])
+        self._shape = (n, h, w)
         if self.build_mode == "replicated" or self.world == 1:
             self.storage = torch.empty((n, h, w, 4), dtype=torch.float32, device=self.dev)
             self.quads = self.storage

@@ -1,0 +1,136 @@
+"""Parity at BASELINE.json's full sizes (configs 2, 3, 4). Needs a B200.
+
+The oracle cannot render a 1024^2 cone frame in test time (~6 CPU-minutes per
+frame at config 3), so full-size frames are checked three ways:
+
+- against the oracle on a stratified subset: light-texel rows of the build
+  (bit-exact) and image pixels of the march (<= 1e-4), the march subset
+  reading the GPU-built stack (itself bit-exact on the checked rows);
+- through size-independent properties of the full result: every layer of
+  the attenuation stack is non-increasing in k and within [0, 1]; image
+  alpha in [0, 1] and premultiplied colour <= alpha-bound; an all-
+  transparent buffer makes ``sbrc_shadow`` equal ``none``;
+- partition invariance: the frame split into 4 ranks' bands reassembles to
+  the same bits.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, parity_stats
+
+pytestmark = pytest.mark.gpu
+
+sys.path.insert(0, ROOT)
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+    import paper_2008_06134_b200 as sb
+    return sb
+
+
+def _scene(cfg_id, mode=None):
+    import bench
+    cfg = bench.CONFIGS[cfg_id]
+    tf, cam, spec, settings = bench.scene_objects(cfg, mode or cfg["mode"])
+    return cfg, tf, cam, spec, settings
+
+
+def _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows, pix, gpu_vol=None):
+    """Shared checks for one full-size frame; returns the parity stats of the subset.
+    ``v`` is the host volume the oracle reads; ``gpu_vol`` (default ``v``) what the GPU reads."""
+    import torch
+    from oracle import slicecast_oracle as O
+    from paper_2008_06134_b200.frame import band_layout
+    gv = v if gpu_vol is None else gpu_vol
+    buf = sb.build_attenuation_buffer(gv, tf, cam, spec)
+    inten = buf.intensity_device
+    # properties of the whole stack
+    assert float(inten.min()) >= 0.0 and float(inten.max()) <= 1.0
+    assert bool((inten[1:] <= inten[:-1]).all())
+    assert bool((inten[0] == 1.0).all())
+    # oracle on light rows: bit-exact
+    want_rows = O.build_intensity(v, tf.lut, cam, spec, rows=build_rows)
+    got_rows = inten[:, build_rows].cpu().numpy()
+    assert np.array_equal(got_rows, want_rows)
+    img = sb.render_device(gv, tf, settings, buf)
+    torch.cuda.synchronize()
+    # properties of the whole image
+    a = img[..., 3]
+    assert float(a.min()) >= 0.0 and float(a.max()) <= 1.0
+    assert bool((img[..., :3] >= 0).all())
+    # oracle on a stratified pixel subset (reads the GPU stack, bit-exact on the rows above)
+    host = sb.AttenuationBuffer(cam, spec, 0.0, inten.cpu().numpy())
+    want = O.render_image(v, tf.lut, settings, host, rows=pix, cols=pix)
+    got = img.cpu().numpy()[np.ix_(pix, pix)]
+    st = parity_stats(got, want)
+    print(f"[scale] {cfg['name']}: subset {len(pix)}x{len(pix)} max_abs={st['max_abs']:.3e} psnr={st['psnr']:.1f}")
+    assert st["max_abs"] <= 1e-4
+    # partition invariance across 4 ranks
+    h = settings.viewport[1]
+    rows, perm = band_layout(h, 8, 4)
+    parts = []
+    for r in range(4):
+        p = sb.render_device(gv, tf, settings, buf, rank=r, world=4, band_rows=8)
+        pad = rows - p.shape[0]
+        parts.append(torch.nn.functional.pad(p, (0, 0, 0, 0, 0, pad)) if pad else p)
+    assert torch.equal(torch.cat(parts)[torch.from_numpy(perm).to(img.device)], img)
+    return st
+
+
+def test_config2_full_size(sb):
+    import bench
+    cfg, tf, cam, spec, settings = _scene(2)
+    v = bench.host_volume(cfg)  # 256^3 u8 perforated block through the raw round trip
+    assert v.scalar_type == "u8"
+    _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows=np.array([0, 77, 255, 256, 400, 511]),
+                      pix=np.arange(5, 512, 32))
+
+
+def test_config3_full_size(sb):
+    import bench
+    cfg, tf, cam, spec, settings = _scene(3)
+    v = bench.host_volume(cfg)  # 512^3 float32 blobs (numpy, bit-identical to the reference generator)
+    _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows=np.array([3, 200, 256, 511]),
+                      pix=np.arange(7, 1024, 64))
+
+
+def test_config3_transparent_buffer_equals_none(sb):
+    """Acceptance C1 at full size: sbrc_shadow with an all-transparent stack equals none (<= 1e-6)."""
+    import bench
+    import torch
+    from paper_2008_06134_b200.device import DeviceVolume
+    cfg, tf, cam, spec, settings = _scene(3, "sbrc_shadow")
+    dvol, _ = bench.device_volume_for(cfg, torch.device("cuda"))
+    clear = sb.TransferFunction([(0.0, (0, 0, 0, 0)), (1.0, (0.5, 0.5, 0.5, 0.0))])
+    buf = sb.build_attenuation_buffer(dvol, clear, cam, spec)
+    assert bool((buf.intensity_device == 1.0).all())
+    s_none = sb.RenderSettings(camera=settings.camera, light=settings.light, viewport=settings.viewport,
+                               step=settings.step, shading_mode="none")
+    a = sb.render_device(dvol, tf, s_none)
+    b = sb.render_device(dvol, tf, settings, buf)
+    assert float((a - b).abs().max()) <= 1e-6
+
+
+@pytest.mark.skipif(os.environ.get("SBRC_SKIP_CONFIG4") == "1", reason="SBRC_SKIP_CONFIG4=1")
+def test_config4_full_size(sb):
+    """1024^3 u16 volume generated on the GPU; the oracle reads a host copy."""
+    import bench
+    import torch
+    from paper_2008_06134_b200.scene import VolumeDataset
+    cfg, tf, cam, spec, settings = _scene(4)
+    dvol, _ = bench.device_volume_for(cfg, torch.device("cuda"))
+    raw = dvol.data.cpu().numpy().view(np.uint16)
+    v = VolumeDataset.from_raw_array(raw)
+    del raw
+    _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows=np.array([0, 511, 1023]),
+                      pix=np.arange(11, 2048, 256), gpu_vol=dvol)
