@@ -140,7 +140,8 @@ typedef struct sbrc_render_params {
   double cone_cos[SBRC_MAX_ANGLES], cone_sin[SBRC_MAX_ANGLES];
   /* image-space partition: rows grouped in bands of band_rows; band b is
    * rendered by rank b % world into rank-local row (b / world)*band_rows + r */
-  int32_t band_rows, rank, world, _pad2;
+  int32_t band_rows, rank, world;
+  int32_t local_rows;              /* set by the library (rank-local row count) */
   float* image;                    /* device, rank-local (rows, W, 4) premultiplied rgba */
   unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
 } sbrc_render_params;

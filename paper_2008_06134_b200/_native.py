@@ -64,7 +64,7 @@ class SbrcRenderParams(C.Structure):
                 ("shell_radius", C.c_double * MAX_SHELLS), ("shell_weight", C.c_double * MAX_SHELLS),
                 ("cone_ring", C.c_double), ("cone_cos", C.c_double * MAX_ANGLES),
                 ("cone_sin", C.c_double * MAX_ANGLES),
-                ("band_rows", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("_pad2", C.c_int32),
+                ("band_rows", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("local_rows", C.c_int32),
                 ("image", C.c_void_p), ("sample_count", C.c_void_p)]
 
 

@@ -376,6 +376,9 @@ struct ShellTap {
   float dtx, dty, dli, w;  // texel-space offset of +radius along one world axis; shell weight
 };
 
+#ifndef SBRC_TILE_W
+#define SBRC_TILE_W 8  // warp pixel tile width (8 x 4)
+#endif
 #ifndef SBRC_MARCH_PREFETCH
 #define SBRC_MARCH_PREFETCH 1
 #endif
@@ -436,13 +439,15 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
   }
   __syncthreads();
 
-  // Pixel of this lane: a block is 32 x 8 pixels, each warp an 8 x 4 tile.
+  // Pixel of this lane: each warp owns a TILE_W x (32/TILE_W) pixel tile, a
+  // block 4 x 2 warp tiles.
+  constexpr int TW = SBRC_TILE_W, TH = 32 / SBRC_TILE_W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int px = blockIdx.x * 32 + (warp & 3) * 8 + (lane & 7);
-  const int lr = blockIdx.y * 8 + (warp >> 2) * 4 + (lane >> 3);  // rank-local row
+  const int px = blockIdx.x * (4 * TW) + (warp & 3) * TW + (lane % TW);
+  const int lr = blockIdx.y * (2 * TH) + (warp >> 2) * TH + (lane / TW);  // rank-local row
   const int band = lr / P.band_rows;
   const int py = (P.rank + band * P.world) * P.band_rows + (lr - band * P.band_rows);
-  const bool in_image = px < P.width;  // lr < local rows by construction of the grid
+  const bool in_image = px < P.width && lr < P.local_rows;
   const bool valid = in_image && py < P.height;
 
   unsigned int samples = 0;
@@ -773,9 +778,11 @@ void launch_build(const sbrc_build_params& p, cudaStream_t s) {
 
 template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN>
 void launch_march(const sbrc_render_params& p, cudaStream_t s) {
-  const int rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
-  dim3 grid((p.width + 31) / 32, (rows + 7) / 8);
-  march_kernel<SH, LK, VT, UNIT, NS, CA, CN><<<grid, 256, 0, s>>>(p);
+  constexpr int BW = 4 * SBRC_TILE_W, BH = 2 * (32 / SBRC_TILE_W);
+  sbrc_render_params q = p;
+  q.local_rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
+  dim3 grid((p.width + BW - 1) / BW, (q.local_rows + BH - 1) / BH);
+  march_kernel<SH, LK, VT, UNIT, NS, CA, CN><<<grid, 256, 0, s>>>(q);
 }
 
 template <int SH, int LK, int VT, bool UNIT>
