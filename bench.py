@@ -546,7 +546,8 @@ def load_traffic(config, mode, kernel):
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(f"config{config}/{mode}/{kernel}")
+        e = d.get(f"config{config}/{mode}/{kernel}")
+        return None if e is None else e["bytes"]
     except (OSError, ValueError):
         return None
 

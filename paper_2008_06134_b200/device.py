@@ -116,7 +116,20 @@ def device_volume(v, device=None) -> DeviceVolume:
 
 
 def f64_tensor(arr, device) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
+    """float64 host array -> device, staged through pinned memory and copied
+    asynchronously on the current stream (the pinned block is recycled by
+    torch's caching host allocator once the copy has completed)."""
+    host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))
+    return host.pin_memory().to(device, non_blocking=True)
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> new numpy array via a pinned buffer (fast D2H); the
+    array owns the pinned block until it is garbage collected."""
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out.numpy()
 
 
 def light_frame(cam, spec, offsets_dev: torch.Tensor | None) -> N.SbrcLightFrame:

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import _require_cuda, build_params, current_stream_handle, device_volume, f64_tensor, pack_quads
+from .device import _require_cuda, build_params, current_stream_handle, device_volume, f64_tensor, pack_quads, to_host
 
 
 class AttenuationBuffer:
@@ -42,7 +42,7 @@ class AttenuationBuffer:
     def intensity(self) -> np.ndarray:
         """(n, H, W) float32 numpy stack, as the reference returns it."""
         if self._host is None:
-            self._host = self.intensity_device.cpu().numpy()
+            self._host = to_host(self.intensity_device.contiguous())
         return self._host
 
     @intensity.setter

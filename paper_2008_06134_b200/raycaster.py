@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import _require_cuda, current_stream_handle, device_volume, f64_tensor, pack_quads, render_params
+from .device import _require_cuda, current_stream_handle, device_volume, f64_tensor, pack_quads, render_params, to_host
 from .lightbuffer import AttenuationBuffer
 from .scene import BUFFER_MODES, ConfigError
 
@@ -69,4 +69,4 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
 def render(v, tf, settings, buffer=None) -> np.ndarray:
     """GPU ray cast; drop-in for raycaster.py:443-469 (returns numpy float32 (H, W, 4))."""
     img = render_device(v, tf, settings, buffer)
-    return img.cpu().numpy()
+    return to_host(img)
