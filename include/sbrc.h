@@ -61,7 +61,9 @@ typedef enum sbrc_shading {
   SBRC_SHADE_NONE = 0,   /* "none"        raycaster.py:383-384 */
   SBRC_SHADE_SHADOW = 1, /* "sbrc_shadow" raycaster.py:398-401 */
   SBRC_SHADE_SHELL = 2,  /* "shell"       raycaster.py:402-406 */
-  SBRC_SHADE_CONE = 3    /* "cone"        raycaster.py:407-411 */
+  SBRC_SHADE_CONE = 3,   /* "cone"        raycaster.py:407-411 */
+  SBRC_SHADE_PHONG = 4,  /* "phong"       raycaster.py:204-228, :385-388 (no buffer) */
+  SBRC_SHADE_EXTINCTION = 5 /* "extinction" raycaster.py:312-332, :389-394 (no buffer) */
 } sbrc_shading;
 
 typedef enum sbrc_lookup {
@@ -142,6 +144,10 @@ typedef struct sbrc_render_params {
    * rendered by rank b % world into rank-local row (b / world)*band_rows + r */
   int32_t band_rows, rank, world;
   int32_t local_rows;              /* set by the library (rank-local row count) */
+  /* phong / extinction (settings.light, not the buffer's light) */
+  double scene_light_dir[3];       /* Light.direction (normalised)        */
+  double phong[4];                 /* PhongParams: ambient, diffuse, specular, shininess */
+  double voxel_size[3];            /* VolumeDataset.voxel_size (gradient steps, volume.py:210) */
   float* image;                    /* device, rank-local (rows, W, 4) premultiplied rgba */
   unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
 } sbrc_render_params;
@@ -171,6 +177,13 @@ int sbrc_render(const sbrc_render_params* p, void* stream);
 int sbrc_pack_quads(const float* plain, int64_t plain_layer_stride, int64_t plain_row_stride,
                     int n, int height, int width, float* quads, int64_t quad_layer_stride,
                     int64_t quad_row_stride, void* stream);
+
+/* GPU shadow_oracle_many (raycaster.py:335-366): transmittance from each of
+ * m float64 points pts[3*i..] toward the light, a straight march with
+ * step-corrected opacity: out[i] = prod (1 - min(a, 1 - 1e-6)).
+ * alpha_lut = tf.resolve(oracle_step)[:, 3]; to_light = -light.direction. */
+int sbrc_shadow_oracle(const sbrc_volume* v, const double* alpha_lut, const double* pts, int64_t m,
+                       const double* to_light, double step, double* out, void* stream);
 
 /* Number of rank-local image rows sbrc_render writes for (height, band_rows, rank, world). */
 int sbrc_local_rows(int height, int band_rows, int rank, int world);

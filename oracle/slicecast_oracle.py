@@ -22,6 +22,10 @@ the same float64 operation order so that results agree bit for bit:
 - ``box_hit``            geometry.py:46-67
 - ``march``              raycaster.py:415-440 (_march_rays) with _make_shader :376-412
 - ``render_image``       raycaster.py:443-469
+- ``gradient``           volume.py:201-220 (gradient_many)
+- ``phong_scalar``       raycaster.py:204-220
+- ``light_march``        raycaster.py:312-353 (_extinction_scalar, _shadow_oracle_scalar)
+- ``shadow_oracle``      raycaster.py:356-366 (shadow_oracle_many)
 
 Deliberate restatement choices (semantics-neutral):
 the build evaluates every texel of each slice instead of the polygon's
@@ -282,13 +286,94 @@ def box_hit(origins: np.ndarray, dirs: np.ndarray):
     return t_in, t_out, t_out > t_in
 
 
-def make_shader(vol, settings, buffer):
-    """pts (M,3) -> rgb factor (M,3) for the GPU modes (raycaster.py:376-412)."""
+ALPHA_MAX = 1.0 - 1e-6
+
+
+def gradient(vol, pts) -> np.ndarray:
+    """Central differences, probes clamped to the cube, divided by the actual
+    probe separation (volume.py:201-220)."""
+    q = np.asarray(pts, dtype=np.float64).reshape(-1, 3)
+    h = (vol.box_hi - vol.box_lo) / np.array(vol.dims, dtype=np.float64)
+    g = np.empty_like(q)
+    for a in range(3):
+        d = np.zeros(3)
+        d[a] = h[a]
+        up = np.clip(q + d, 0.0, 1.0)
+        dn = np.clip(q - d, 0.0, 1.0)
+        sep = up[:, a] - dn[:, a]
+        sep = np.where(sep == 0.0, 1.0, sep)
+        g[:, a] = (trilinear(vol, up) - trilinear(vol, dn)) / sep
+    return g.reshape(np.asarray(pts).shape)
+
+
+def phong_scalar(vol, pts, light_dir, eye, ambient, diffuse, specular, shininess) -> np.ndarray:
+    """ambient + diffuse*max(0,N.L) + specular*max(0,R.V)^n (raycaster.py:204-220)."""
+    g = gradient(vol, pts)
+    mag = np.linalg.norm(g, axis=-1)
+    lit = mag > 1e-12
+    res = np.full(pts.shape[0], ambient, dtype=np.float64)
+    if lit.any():
+        nrm = -g[lit] / mag[lit][:, None]
+        tl = -np.asarray(light_dir, dtype=np.float64)
+        ndl = np.maximum(0.0, nrm @ tl)
+        view = eye - pts[lit]
+        view /= np.linalg.norm(view, axis=-1, keepdims=True)
+        refl = 2.0 * ndl[:, None] * nrm - tl
+        rdv = np.maximum(0.0, np.sum(refl * view, axis=-1))
+        res[lit] += diffuse * ndl + specular * np.power(rdv, shininess)
+    return res
+
+
+def light_march(vol, alpha_lut, pts, to_light, step, extinction: bool) -> np.ndarray:
+    """March from each point toward the light: sum of -log1p(-a) (extinction,
+    raycaster.py:312-332) or the product of (1 - a) (oracle, :335-353), with
+    a = min(lut(trilinear), ALPHA_MAX)."""
+    m = pts.shape[0]
+    t_in, t_out, hit = box_hit(pts, np.broadcast_to(to_light, (m, 3)))
+    acc = np.zeros(m) if extinction else np.ones(m)
+    live = np.flatnonzero(hit)
+    t = t_in[live] + 0.5 * step
+    t_end = t_out[live]
+    while live.size:
+        keep = t < t_end
+        live, t, t_end = live[keep], t[keep], t_end[keep]
+        if not live.size:
+            break
+        a = lut_blend(alpha_lut[:, None], trilinear(vol, pts[live] + t[:, None] * to_light))[:, 0]
+        if extinction:
+            acc[live] += -np.log1p(-np.minimum(a, ALPHA_MAX))
+        else:
+            acc[live] *= 1.0 - np.minimum(a, ALPHA_MAX)
+        t = t + step
+    return acc
+
+
+def shadow_oracle(vol, tf_lut, pts, light_dir, oracle_step) -> np.ndarray:
+    """Brute-force transmittance to the light (raycaster.py:356-366)."""
+    alpha = resolve(tf_lut, oracle_step)[:, 3]
+    p = np.asarray(pts, dtype=np.float64)
+    return light_march(vol, alpha, p.reshape(-1, 3), -np.asarray(light_dir, dtype=np.float64), oracle_step,
+                       False).reshape(p.shape[:-1])
+
+
+def make_shader(vol, settings, buffer, alpha_lut_step=None):
+    """pts (M,3) -> rgb factor (M,3) (raycaster.py:376-412)."""
     mode = settings.shading_mode
     if mode == "none":
         return lambda p: np.ones((p.shape[0], 3), dtype=np.float64)
+    if mode == "phong":
+        ph = settings.phong
+        eye = np.asarray(settings.camera.position, dtype=np.float64)
+        ld = settings.light.direction
+        return lambda p: np.repeat(phong_scalar(vol, p, ld, eye, ph.ambient, ph.diffuse, ph.specular,
+                                                ph.shininess)[:, None], 3, axis=1)
+    if mode == "extinction":
+        tl = -np.asarray(settings.light.direction, dtype=np.float64)
+        fl = settings.ambient_floor
+        return lambda p: np.repeat(np.maximum(np.exp(-light_march(vol, alpha_lut_step, p, tl, settings.step, True)),
+                                              fl)[:, None], 3, axis=1)
     if mode not in ("sbrc_shadow", "shell", "cone"):
-        raise ValueError(f"mode {mode!r} is outside the oracle's scope")
+        raise ValueError(f"unknown shading mode {mode!r}")
     inten = np.asarray(buffer.intensity)
     cam, spec = buffer.camera, buffer.spec
     color = np.asarray(buffer.camera.light_color, dtype=np.float64)
@@ -360,7 +445,7 @@ def render_image(vol, tf_lut: np.ndarray, settings, buffer=None, rows=None, cols
         dirs = dirs[:, np.asarray(cols)]
     hh, ww = dirs.shape[:2]
     flat, samples = march(vol, lut, settings.step, settings.early_termination_alpha,
-                          make_shader(vol, settings, buffer), np.asarray(cam.position, np.float64),
-                          dirs.reshape(-1, 3))
+                          make_shader(vol, settings, buffer, np.ascontiguousarray(lut[:, 3])),
+                          np.asarray(cam.position, np.float64), dirs.reshape(-1, 3))
     img = flat.reshape(hh, ww, 4).astype(np.float32)
     return (img, samples) if return_samples else img

@@ -29,5 +29,5 @@ from .scene import (  # noqa: F401
     preset,
 )
 from .lightbuffer import AttenuationBuffer, build_attenuation_buffer  # noqa: F401
-from .raycaster import render, render_device  # noqa: F401
+from .raycaster import render, render_device, shadow_oracle_many  # noqa: F401
 from .device import DeviceVolume, device_volume  # noqa: F401

@@ -22,12 +22,12 @@ MAX_ANGLES = 16
 
 OK, EINVAL, ECONFIG, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4
 VOXEL_F32, VOXEL_U8, VOXEL_U16, VOXEL_F64 = 0, 1, 2, 3
-SHADE = {"none": 0, "sbrc_shadow": 1, "shell": 2, "cone": 3}
+SHADE = {"none": 0, "sbrc_shadow": 1, "shell": 2, "cone": 3, "phong": 4, "extinction": 5}
 LOOKUP = {"linear": 0, "nearest": 1}
 
 #: every symbol include/sbrc.h declares
 EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume_check",
-           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_local_rows")
+           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_shadow_oracle", "sbrc_local_rows")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -65,6 +65,7 @@ class SbrcRenderParams(C.Structure):
                 ("cone_ring", C.c_double), ("cone_cos", C.c_double * MAX_ANGLES),
                 ("cone_sin", C.c_double * MAX_ANGLES),
                 ("band_rows", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("local_rows", C.c_int32),
+                ("scene_light_dir", D3), ("phong", C.c_double * 4), ("voxel_size", D3),
                 ("image", C.c_void_p), ("sample_count", C.c_void_p)]
 
 
@@ -83,6 +84,8 @@ def _load() -> C.CDLL:
     lib.sbrc_build.argtypes = [C.POINTER(SbrcBuildParams), C.c_void_p]
     lib.sbrc_render.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p]
     lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    lib.sbrc_shadow_oracle.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                       C.c_double, C.c_void_p, C.c_void_p]
     lib.sbrc_pack_quads.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
                                     C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
     if lib.sbrc_abi_version() != ABI_VERSION:

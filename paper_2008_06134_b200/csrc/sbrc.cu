@@ -311,6 +311,95 @@ __global__ void __launch_bounds__(256) pack_quads_kernel(const float* __restrict
   emit_pair(row + (size_t)(n - 1) * (size_t)qk, x, w, prev, prev);
 }
 
+// ---------------------------------------------------------------- rays
+// ray_box_intersect (geometry.py:46-67) for one ray: slab test against the
+// unit cube with the reference's parallel-ray handling; t_enter = max(t_near, 0).
+__device__ __forceinline__ bool box_hit(const double o[3], const double d[3], double& t_enter, double& t_far) {
+  double t_near = -INFINITY;
+  t_far = INFINITY;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double lo, hi;
+    if (d[c] == 0.0) {
+      const bool inside = in01(o[c]);
+      lo = inside ? -INFINITY : INFINITY;
+      hi = inside ? INFINITY : -INFINITY;
+    } else {
+      const double inv = ddiv(1.0, d[c]);
+      lo = dmul(dsub(0.0, o[c]), inv);
+      hi = dmul(dsub(1.0, o[c]), inv);
+    }
+    t_near = fmax(t_near, fmin(lo, hi));
+    t_far = fmin(t_far, fmax(lo, hi));
+  }
+  t_enter = fmax(t_near, 0.0);
+  return t_far > t_enter;
+}
+
+// ALPHA_MAX = 1 - 1e-6 (raycaster.py:34)
+#define SBRC_ALPHA_MAX (1.0 - 1e-6)
+
+// Straight march from p toward the light (raycaster.py:312-353): EXT returns
+// sum(-log1p(-min(a, ALPHA_MAX))) (_extinction_scalar), otherwise
+// prod(1 - min(a, ALPHA_MAX)) (_shadow_oracle_scalar). Float64, reference op
+// order; only log1p's last ulp can differ from glibc's.
+template <int VT, bool UNIT, bool EXT>
+__device__ double light_march(const sbrc_volume& v, const double* alut, const float* u8tab, const double p[3],
+                              const double tl[3], double step) {
+  double t_enter, t_far;
+  if (!box_hit(p, tl, t_enter, t_far)) return EXT ? 0.0 : 1.0;
+  double acc = EXT ? 0.0 : 1.0;
+  for (double t = dadd(t_enter, 0.5 * step); t < t_far; t = dadd(t, step)) {
+    const double s = trilinear64<VT, UNIT>(v, u8tab, dadd(p[0], dmul(t, tl[0])), dadd(p[1], dmul(t, tl[1])),
+                                           dadd(p[2], dmul(t, tl[2])));
+    const LutPos q = lut_pos(s);
+    const double a = fmin(dadd(dmul(alut[q.i0], q.g), dmul(alut[q.i1], q.f)), SBRC_ALPHA_MAX);
+    if (EXT) acc = dadd(acc, -log1p(-a));
+    else acc = dmul(acc, dsub(1.0, a));
+  }
+  return acc;
+}
+
+// _phong_scalar (raycaster.py:204-220) with gradient_many (volume.py:201-220):
+// central differences with probes clamped to the cube, divided by the actual
+// probe separation; the lit test |g| > 1e-12 sees the same float64 gradient.
+template <int VT, bool UNIT>
+__device__ double phong_scalar(const sbrc_render_params& P, const float* u8tab, const double p[3]) {
+  double g[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double hi[3] = {dclip01(p[0]), dclip01(p[1]), dclip01(p[2])};
+    double lo[3] = {hi[0], hi[1], hi[2]};
+    hi[a] = dclip01(dadd(p[a], P.voxel_size[a]));
+    lo[a] = dclip01(dsub(p[a], P.voxel_size[a]));
+    double sep = dsub(hi[a], lo[a]);
+    if (sep == 0.0) sep = 1.0;
+    g[a] = ddiv(dsub(trilinear64<VT, UNIT>(P.volume, u8tab, hi[0], hi[1], hi[2]),
+                     trilinear64<VT, UNIT>(P.volume, u8tab, lo[0], lo[1], lo[2])), sep);
+  }
+  const double norm = __dsqrt_rn(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
+  const double ambient = P.phong[0];
+  if (!(norm > 1e-12)) return ambient;
+  double n[3], view[3];
+  double vn = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    n[c] = ddiv(-g[c], norm);
+    view[c] = dsub(P.eye[c], p[c]);
+    vn += view[c] * view[c];
+  }
+  vn = sqrt(vn);
+  double ndl = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) ndl += n[c] * -P.scene_light_dir[c];
+  ndl = fmax(0.0, ndl);
+  double rdv = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) rdv += (2.0 * ndl * n[c] + P.scene_light_dir[c]) * (view[c] / vn);
+  rdv = fmax(0.0, rdv);
+  return ambient + (P.phong[1] * ndl + P.phong[2] * pow(rdv, P.phong[3]));
+}
+
 // ---------------------------------------------------------------- K2 march
 // Light-space lookup state. Texel coordinates tx = u*W - 0.5, ty = v*H - 0.5
 // and the layer coordinate li = idx - 0.5 (lightbuffer.py:241-242, :279).
@@ -392,8 +481,11 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
   __shared__ double u8tab[256];
+  __shared__ double alut[SHADING == SBRC_SHADE_EXTINCTION ? SBRC_LUT_SIZE : 1];
   for (int i = threadIdx.x; i < SBRC_LUT_SIZE * 2; i += blockDim.x)
     lut[i] = reinterpret_cast<const double2*>(P.lut_rgba)[i];
+  if (SHADING == SBRC_SHADE_EXTINCTION)
+    for (int i = threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x) alut[i] = P.lut_rgba[4 * i + 3];
   if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
 
   const sbrc_light_frame& LF = P.light;
@@ -489,7 +581,8 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
       double tx0 = 0, txd = 0, ty0 = 0, tyd = 0, li0 = 0, lid = 0;
       float cbu = 1.0f, cbv = 0.0f, dperp = 0.0f;
       float fr_c = 1.f, fg_c = 1.f, fb_c = 1.f, ir = 1.f, ig = 1.f, ib = 1.f;
-      if (SHADING != SBRC_SHADE_NONE) {
+      constexpr bool BUFFERED = SHADING == SBRC_SHADE_SHADOW || SHADING == SBRC_SHADE_SHELL || SHADING == SBRC_SHADE_CONE;
+      if (BUFFERED) {
         tex.q = reinterpret_cast<const float4*>(P.quads);
         tex.qk = (unsigned)P.quad_layer_stride;
         tex.qy = (unsigned)P.quad_row_stride;
@@ -604,7 +697,20 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
         const double sa = dadd(dmul(a_ba.y, q.g), dmul(b_ba.y, q.f));
 
         double fr = 1.0, fg = 1.0, fb = 1.0;
-        if (SHADING != SBRC_SHADE_NONE) {
+        if (SHADING == SBRC_SHADE_PHONG || SHADING == SBRC_SHADE_EXTINCTION) {
+          const double p[3] = {dadd(P.eye[0], dmul(t, d[0])), dadd(P.eye[1], dmul(t, d[1])),
+                               dadd(P.eye[2], dmul(t, d[2]))};
+          double f;
+          if (SHADING == SBRC_SHADE_PHONG) {
+            f = phong_scalar<VT, UNIT>(P, reinterpret_cast<const float*>(u8tab), p);  // raycaster.py:385-388
+          } else {  // raycaster.py:389-394: max(exp(-tau), floor), alpha LUT at settings.step
+            const double tl[3] = {-P.scene_light_dir[0], -P.scene_light_dir[1], -P.scene_light_dir[2]};
+            const double tau = light_march<VT, UNIT, true>(P.volume, alut, reinterpret_cast<const float*>(u8tab),
+                                                          p, tl, step);
+            f = fmax(exp(-tau), (double)P.ambient_floor);
+          }
+          fr = fg = fb = f;
+        } else if (SHADING != SBRC_SHADE_NONE) {
           const float tx = fmaf(jf, ftxs, ftx0);
           const float ty = fmaf(jf, ftys, fty0);
           const float li = fmaf(jf, flis, fli0);
@@ -739,6 +845,23 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
   }
 }
 
+// GPU shadow_oracle_many (raycaster.py:356-366): one thread per point.
+template <int VT, bool UNIT>
+__global__ void __launch_bounds__(256) shadow_oracle_kernel(const sbrc_volume V, const double* __restrict__ alpha_lut,
+                                                            const double* __restrict__ pts, int64_t m, double tl0,
+                                                            double tl1, double tl2, double step, double* out) {
+  __shared__ double alut[SBRC_LUT_SIZE];
+  __shared__ double u8tab[256];
+  for (int i = threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x) alut[i] = alpha_lut[i];
+  if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+  const double tl[3] = {tl0, tl1, tl2};
+  out[i] = light_march<VT, UNIT, false>(V, alut, reinterpret_cast<const float*>(u8tab), p, tl, step);
+}
+
 // ---------------------------------------------------------------- dispatch
 bool volume_ok(const sbrc_volume& v) {
   if (v.data == nullptr) return false;
@@ -813,7 +936,8 @@ void launch_march_vt(const sbrc_render_params& p, cudaStream_t s) {
 }
 template <int SH>
 void launch_march_lookup(const sbrc_render_params& p, cudaStream_t s) {
-  if (SH != SBRC_SHADE_NONE && p.lookup == SBRC_LOOKUP_NEAREST) launch_march_vt<SH, SBRC_LOOKUP_NEAREST>(p, s);
+  if ((SH == SBRC_SHADE_SHADOW || SH == SBRC_SHADE_SHELL || SH == SBRC_SHADE_CONE) && p.lookup == SBRC_LOOKUP_NEAREST)
+    launch_march_vt<SH, SBRC_LOOKUP_NEAREST>(p, s);
   else launch_march_vt<SH, SBRC_LOOKUP_LINEAR>(p, s);
 }
 
@@ -882,16 +1006,40 @@ int sbrc_pack_quads(const float* plain, int64_t plain_layer_stride, int64_t plai
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 
+int sbrc_shadow_oracle(const sbrc_volume* v, const double* alpha_lut, const double* pts, int64_t m,
+                       const double* to_light, double step, double* out, void* stream) {
+  if (v == nullptr || !volume_ok(*v) || alpha_lut == nullptr || to_light == nullptr || out == nullptr)
+    return SBRC_EINVAL;
+  if (!(step > 0.0) || m < 0 || (m > 0 && pts == nullptr)) return SBRC_EINVAL;  // raycaster.py:361-362
+  if (m == 0) return SBRC_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned blocks = (unsigned)((m + 255) / 256);
+  const bool unit = unit_box(*v);
+#define SBRC_ORACLE(VT)                                                                                        \
+  (unit ? shadow_oracle_kernel<VT, true><<<blocks, 256, 0, s>>>(*v, alpha_lut, pts, m, to_light[0], to_light[1], \
+                                                                to_light[2], step, out)                        \
+        : shadow_oracle_kernel<VT, false><<<blocks, 256, 0, s>>>(*v, alpha_lut, pts, m, to_light[0], to_light[1], \
+                                                                 to_light[2], step, out))
+  switch (v->voxel_type) {
+    case SBRC_VOXEL_F32: SBRC_ORACLE(SBRC_VOXEL_F32); break;
+    case SBRC_VOXEL_F64: SBRC_ORACLE(SBRC_VOXEL_F64); break;
+    case SBRC_VOXEL_U8: SBRC_ORACLE(SBRC_VOXEL_U8); break;
+    default: SBRC_ORACLE(SBRC_VOXEL_U16); break;
+  }
+#undef SBRC_ORACLE
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
 int sbrc_render(const sbrc_render_params* p, void* stream) {
   if (p == nullptr || !volume_ok(p->volume)) return SBRC_EINVAL;
   if (p->width < 1 || p->height < 1 || !(p->step > 0.0)) return SBRC_EINVAL;           // raycaster.py:143-146
   if (!(p->et_alpha > 0.0 && p->et_alpha <= 1.0)) return SBRC_EINVAL;                  // :147-148
   if (p->lut_rgba == nullptr || p->image == nullptr) return SBRC_EINVAL;
-  if (p->shading < SBRC_SHADE_NONE || p->shading > SBRC_SHADE_CONE) return SBRC_EUNSUPPORTED;
+  if (p->shading < SBRC_SHADE_NONE || p->shading > SBRC_SHADE_EXTINCTION) return SBRC_EUNSUPPORTED;
   if (p->lookup != SBRC_LOOKUP_LINEAR && p->lookup != SBRC_LOOKUP_NEAREST) return SBRC_EINVAL;
   if (p->band_rows < 1 || p->band_rows % 8 != 0 || p->world < 1 || p->rank < 0 || p->rank >= p->world)
     return SBRC_EINVAL;
-  if (p->shading != SBRC_SHADE_NONE) {
+  if (p->shading >= SBRC_SHADE_SHADOW && p->shading <= SBRC_SHADE_CONE) {
     if (p->quads == nullptr) return SBRC_ECONFIG;
     if (!light_ok(p->light)) return SBRC_EINVAL;
     if (!quads_ok(p->light, p->quad_layer_stride, p->quad_row_stride)) return SBRC_EINVAL;
@@ -906,6 +1054,8 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (p->shading) {
     case SBRC_SHADE_NONE: launch_march_lookup<SBRC_SHADE_NONE>(*p, s); break;
+    case SBRC_SHADE_PHONG: launch_march_lookup<SBRC_SHADE_PHONG>(*p, s); break;
+    case SBRC_SHADE_EXTINCTION: launch_march_lookup<SBRC_SHADE_EXTINCTION>(*p, s); break;
     case SBRC_SHADE_SHADOW: launch_march_lookup<SBRC_SHADE_SHADOW>(*p, s); break;
     case SBRC_SHADE_SHELL: launch_march_lookup<SBRC_SHADE_SHELL>(*p, s); break;
     default: launch_march_lookup<SBRC_SHADE_CONE>(*p, s); break;

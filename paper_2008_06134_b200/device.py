@@ -185,12 +185,11 @@ def pack_quads(plain: torch.Tensor, quads: torch.Tensor | None = None) -> torch.
 def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_cam, buffer_spec,
                   quads_dev: torch.Tensor | None, light_color, voxel_size_max: float,
                   image: torch.Tensor, counter: torch.Tensor | None,
-                  band_rows: int = 8, rank: int = 0, world: int = 1) -> N.SbrcRenderParams:
+                  band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469)."""
     mode = settings.shading_mode
     if mode not in N.SHADE:
-        raise ValueError(f"shading mode {mode!r} is not part of the GPU hot path "
-                         "(supported: none, sbrc_shadow, shell, cone)")
+        raise ValueError(f"unknown shading mode {mode!r}")
     if settings.lookup_mode not in N.LOOKUP:
         raise ValueError(f"unknown lookup mode {settings.lookup_mode!r}")
     p = N.SbrcRenderParams()
@@ -209,12 +208,18 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     p.tan_half, p.aspect = fr["tan_half"], fr["aspect"]
     p.step = float(settings.step)
     p.et_alpha = float(settings.early_termination_alpha)
-    if mode != "none":
+    if mode in ("sbrc_shadow", "shell", "cone"):
         p.light = light_frame(buffer_cam, buffer_spec, None)
         if quads_dev is not None:
             p.quads = quads_dev.data_ptr()
             p.quad_layer_stride, p.quad_row_stride = quad_strides(quads_dev)
         p.light_color[:] = [float(c) for c in np.asarray(light_color, dtype=np.float64)]
+        p.ambient_floor = float(settings.ambient_floor)
+    if mode in ("phong", "extinction"):
+        p.scene_light_dir[:] = [float(x) for x in np.asarray(settings.light.direction, dtype=np.float64)]
+        ph = settings.phong
+        p.phong[:] = [float(ph.ambient), float(ph.diffuse), float(ph.specular), float(ph.shininess)]
+        p.voxel_size[:] = [float(x) for x in voxel_size]
         p.ambient_floor = float(settings.ambient_floor)
     if mode == "shell":
         k = settings.shell_kernel or ShellKernel.default(float(voxel_size_max))

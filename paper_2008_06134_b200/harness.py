@@ -1,0 +1,238 @@
+"""Callers of the hot path: a device-resident buffer cache and a benchmark sweep.
+
+- ``BufferCache`` mirrors the reference service's bounded LRU with an atomic
+  get-or-build per key (service.py:98-130) and its key (dataset, TF, light
+  direction rounded to 12 digits, light colour, slice count, resolution,
+  compensation; service.py:231-239). Entries are ``AttenuationBuffer``s whose
+  stacks stay in HBM, so a camera-only change costs no build
+  (service.py:246-248: build_ms = 0 on a hit). A byte budget bounds the HBM
+  the cache may hold (a 1024-slice 1024^2 stack is 16 GiB of texel quads).
+- ``run_sweep`` / ``write_csv`` reproduce ``slicecast.bench`` (bench.py:26-146):
+  every (method, n_slices, resolution), ``repeats`` timed runs after one
+  discarded warm-up whose image is hashed, the same CSV columns. Times are
+  device times (CUDA events around the build and the render enqueue).
+"""
+
+from __future__ import annotations
+
+import csv
+import hashlib
+import io
+import json
+import threading
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .lightbuffer import AttenuationBuffer, build_attenuation_buffer
+from .raycaster import render_device
+from .scene import BUFFER_MODES, LightCamera, RenderSettings, make_slice_stack
+
+#: bench/CLI method names -> shading modes (config.py:18-25); "has" is not on the GPU path
+METHOD_MODES = {"none": "none", "phong": "phong", "sbrc": "sbrc_shadow", "shell": "shell", "cone": "cone",
+                "extinction": "extinction"}
+
+CSV_FIELDS = ("method", "n_slices", "buffer_resolution", "sample_step", "build_ms", "render_ms", "total_ms",
+              "pass_count", "image_sha256")
+
+
+def tf_key(tf) -> str:
+    cp = getattr(tf, "control_points", None)
+    if cp is not None:
+        return json.dumps([[x, list(c)] for x, c in cp])
+    return hashlib.sha256(np.ascontiguousarray(tf.lut).tobytes()).hexdigest()
+
+
+def buffer_key(dataset_id, tf, light_dir, light_color, n_slices: int, resolution, compensation_n: float = 0.0):
+    """service.py:231-239."""
+    return (dataset_id, tf_key(tf), tuple(np.round(np.asarray(light_dir, dtype=np.float64), 12)),
+            tuple(float(c) for c in light_color), int(n_slices), tuple(int(r) for r in resolution),
+            float(compensation_n))
+
+
+def _buffer_bytes(buf) -> int:
+    q = getattr(buf, "quads", None)
+    return 0 if q is None else q.numel() * q.element_size()
+
+
+class BufferCache:
+    """Bounded LRU of device-resident attenuation buffers with atomic get-or-build."""
+
+    def __init__(self, max_entries: int = 8, max_bytes: int | None = None):
+        self.max_entries = max_entries
+        self.max_bytes = max_bytes
+        self._entries: OrderedDict = OrderedDict()
+        self._pending: dict = {}
+        self._lock = threading.Lock()
+
+    def __len__(self) -> int:
+        return len(self._entries)
+
+    @property
+    def bytes(self) -> int:
+        return sum(_buffer_bytes(v) for v in self._entries.values())
+
+    def get_or_build(self, key, builder):
+        """(value, hit). Concurrent requests for one key build once; a failed
+        build releases the waiters (service.py:107-130)."""
+        while True:
+            with self._lock:
+                if key in self._entries:
+                    self._entries.move_to_end(key)
+                    return self._entries[key], True
+                event = self._pending.get(key)
+                if event is None:
+                    self._pending[key] = threading.Event()
+                    break
+            event.wait()
+        try:
+            value = builder()
+        except BaseException:
+            with self._lock:
+                self._pending.pop(key).set()
+            raise
+        with self._lock:
+            self._entries[key] = value
+            self._evict()
+            self._pending.pop(key).set()
+        return value, False
+
+    def _evict(self) -> None:
+        while len(self._entries) > self.max_entries:
+            self._entries.popitem(last=False)
+        if self.max_bytes is not None:
+            while len(self._entries) > 1 and self.bytes > self.max_bytes:
+                self._entries.popitem(last=False)
+
+    def clear(self) -> None:
+        with self._lock:
+            self._entries.clear()
+
+
+def cached_build(cache: BufferCache, dataset_id, v, tf, light, n_slices: int, resolution,
+                 compensation_n: float = 0.0) -> tuple[AttenuationBuffer, bool]:
+    """The service's build path (service.py:241-248) over the device cache."""
+    key = buffer_key(dataset_id, tf, light.direction, light.color, n_slices, resolution, compensation_n)
+
+    def _build():
+        cam = LightCamera.fit(light.direction, light.color, resolution)
+        stack = make_slice_stack(light.direction, n_slices)
+        return build_attenuation_buffer(v, tf, cam, stack, compensation_n)
+
+    return cache.get_or_build(key, _build)
+
+
+# ------------------------------------------------------------------ bench sweep
+@dataclass
+class BenchRecord:
+    """One CSV row (bench.py:39-69)."""
+
+    method: str
+    n_slices: int
+    buffer_resolution: tuple
+    sample_step: float
+    build_ms: float
+    render_ms: float
+    pass_count: int
+    image_sha256: str = ""
+
+    def __post_init__(self):
+        if self.build_ms < 0 or self.render_ms < 0:
+            raise ValueError("timings must be >= 0")
+
+    @property
+    def total_ms(self) -> float:
+        return self.build_ms + self.render_ms
+
+    def as_row(self) -> dict:
+        return {"method": self.method, "n_slices": self.n_slices,
+                "buffer_resolution": f"{self.buffer_resolution[0]}x{self.buffer_resolution[1]}",
+                "sample_step": repr(self.sample_step), "build_ms": f"{self.build_ms:.3f}",
+                "render_ms": f"{self.render_ms:.3f}", "total_ms": f"{self.total_ms:.3f}",
+                "pass_count": self.pass_count, "image_sha256": self.image_sha256}
+
+
+def parse_row(row: dict) -> BenchRecord:
+    w, h = row["buffer_resolution"].split("x")
+    return BenchRecord(method=row["method"], n_slices=int(row["n_slices"]), buffer_resolution=(int(w), int(h)),
+                       sample_step=float(row["sample_step"]), build_ms=float(row["build_ms"]),
+                       render_ms=float(row["render_ms"]), pass_count=int(row["pass_count"]),
+                       image_sha256=row["image_sha256"])
+
+
+def image_sha256(img) -> str:
+    """Hash of the float32 (H, W, 4) image bytes, as the reference computes it (bench.py:112-113)."""
+    arr = img.cpu().numpy() if isinstance(img, torch.Tensor) else np.asarray(img)
+    return hashlib.sha256(np.ascontiguousarray(arr, dtype=np.float32).tobytes()).hexdigest()
+
+
+def render_scene(v, tf, settings, method: str, n_slices: int, resolution, compensation_n: float = 0.0):
+    """bench.render_scene (bench.py:87-109) on the device: (image, build_ms, render_ms, pass_count)."""
+    if method not in METHOD_MODES:
+        raise ValueError(f"method {method!r} is not on the GPU path (choose from {sorted(METHOD_MODES)})")
+    mode = METHOD_MODES[method]
+    s = RenderSettings(camera=settings.camera, light=settings.light, viewport=settings.viewport,
+                       step=settings.step, shading_mode=mode,
+                       early_termination_alpha=settings.early_termination_alpha,
+                       ambient_floor=settings.ambient_floor, shell_kernel=settings.shell_kernel,
+                       cone_kernel=settings.cone_kernel, phong=settings.phong, lookup_mode=settings.lookup_mode)
+    stream = torch.cuda.current_stream()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    buf = None
+    e0.record(stream)
+    if mode in BUFFER_MODES:
+        light = settings.light
+        cam = LightCamera.fit(light.direction, light.color, resolution)
+        stack = make_slice_stack(light.direction, n_slices)
+        buf = build_attenuation_buffer(v, tf, cam, stack, compensation_n)
+    e1.record(stream)
+    img = render_device(v, tf, s, buf)
+    e2.record(stream)
+    e2.synchronize()
+    build_ms = e0.elapsed_time(e1) if buf is not None else 0.0
+    return img, build_ms, e1.elapsed_time(e2), 1
+
+
+def run_sweep(v, tf, settings, methods, slices, resolutions, repeats: int = 3) -> list[BenchRecord]:
+    """Every (method, n_slices, resolution); mean of ``repeats`` timed runs after a
+    discarded warm-up whose image is hashed (bench.py:116-146)."""
+    if repeats < 1:
+        raise ValueError("repeats must be >= 1")
+    out = []
+    for method in methods:
+        for n in slices:
+            for res in resolutions:
+                res = (res, res) if isinstance(res, int) else tuple(res)
+                builds, renders, digest = [], [], ""
+                for i in range(repeats + 1):
+                    img, b, r, passes = render_scene(v, tf, settings, method, n, res)
+                    if i == 0:
+                        digest = image_sha256(img)
+                        continue
+                    builds.append(b)
+                    renders.append(r)
+                out.append(BenchRecord(method=method, n_slices=n, buffer_resolution=res,
+                                       sample_step=settings.step, build_ms=float(np.mean(builds)),
+                                       render_ms=float(np.mean(renders)), pass_count=passes, image_sha256=digest))
+    return out
+
+
+def write_csv(records, fh_or_path) -> None:
+    own = isinstance(fh_or_path, (str, bytes)) or hasattr(fh_or_path, "__fspath__")
+    fh = open(fh_or_path, "w", newline="") if own else fh_or_path
+    try:
+        w = csv.DictWriter(fh, fieldnames=CSV_FIELDS)
+        w.writeheader()
+        for rec in records:
+            w.writerow(rec.as_row())
+    finally:
+        if own:
+            fh.close()
+
+
+def csv_text(records) -> str:
+    buf = io.StringIO()
+    write_csv(records, buf)
+    return buf.getvalue()

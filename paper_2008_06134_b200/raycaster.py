@@ -8,11 +8,16 @@ with a transparent-black background. ``render`` returns numpy like the
 reference; ``render_device`` returns the CUDA tensor and optionally the
 executed-sample count.
 
-Modes on the hot path: ``none``, ``sbrc_shadow``, ``shell``, ``cone``.
-``phong`` and ``extinction`` are not part of it and raise.
+Modes: ``none``, ``sbrc_shadow``, ``shell``, ``cone`` (the hot path), and
+``phong`` / ``extinction`` (local lighting with a float64
+central-difference gradient, and a per-sample light march). Also
+``shadow_oracle_many``, the brute-force transmittance the buffer modes are
+measured against (raycaster.py:356-366).
 """
 
 from __future__ import annotations
+
+import ctypes as C
 
 import numpy as np
 import torch
@@ -60,7 +65,7 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
             raise ValueError("attenuation intensity shape does not match its camera/stack")
     vs = float(dvol.voxel_size.max())   # ShellKernel.default(v.voxel_size.max()), :403
     p = render_params(dvol, lut, settings, cam, spec, inten, color, vs, out, counter,
-                      band_rows=band_rows, rank=rank, world=world)
+                      band_rows=band_rows, rank=rank, world=world, voxel_size=dvol.voxel_size)
     N.check(N.lib.sbrc_render(p, current_stream_handle()), "sbrc_render")
     img = out[:h] if world == 1 else out
     return (img, counter) if count_samples else img
@@ -70,3 +75,22 @@ def render(v, tf, settings, buffer=None) -> np.ndarray:
     """GPU ray cast; drop-in for raycaster.py:443-469 (returns numpy float32 (H, W, 4))."""
     img = render_device(v, tf, settings, buffer)
     return to_host(img)
+
+
+def shadow_oracle_many(v, tf, pts, light, oracle_step: float, *, device=None) -> np.ndarray:
+    """GPU shadow_oracle_many (raycaster.py:356-366): transmittance from each
+    (M, 3) world point to the light; returns float64 numpy (M,)."""
+    if oracle_step <= 0:
+        raise ValueError("oracle_step must be positive")
+    dev = _require_cuda(device)
+    dvol = device_volume(v, dev)
+    alpha = f64_tensor(tf.resolve(oracle_step)[:, 3], dev)
+    p = np.ascontiguousarray(np.asarray(pts, dtype=np.float64).reshape(-1, 3))
+    pd = f64_tensor(p, dev)
+    out = torch.empty(p.shape[0], dtype=torch.float64, device=dev)
+    to_light = (C.c_double * 3)(*[-float(x) for x in np.asarray(light.direction, dtype=np.float64)])
+    vs = dvol.struct()
+    N.check(N.lib.sbrc_shadow_oracle(C.byref(vs), alpha.data_ptr(), pd.data_ptr(), p.shape[0], to_light,
+                                     float(oracle_step), out.data_ptr(), current_stream_handle()),
+            "sbrc_shadow_oracle")
+    return to_host(out).reshape(np.asarray(pts).shape[:-1])

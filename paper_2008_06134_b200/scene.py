@@ -336,8 +336,8 @@ class ConeKernel:
 
 BUFFER_MODES = ("sbrc_shadow", "shell", "cone")
 SHADING_MODES = ("none", "phong") + BUFFER_MODES + ("extinction",)
-#: modes this hot path implements on the GPU; the rest raise
-GPU_MODES = ("none",) + BUFFER_MODES
+#: every reference shading mode runs on the GPU
+GPU_MODES = SHADING_MODES
 
 
 @dataclass(frozen=True)

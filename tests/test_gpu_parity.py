@@ -357,3 +357,27 @@ def test_anisotropic_box_general_path(sb):
     assert parity_stats(sb.render(v, tf, s, buf), O.render_image(v, tf.lut, s, buf))["max_abs"] <= TIGHT
     s0 = sb.RenderSettings(camera=s.camera, light=s.light, viewport=(34, 30), step=1 / 50)
     assert np.array_equal(sb.render(v, tf, s0), O.render_image(v, tf.lut, s0))
+
+
+def test_phong_extinction_and_shadow_oracle(sb):
+    """SURVEY §8f row 3 on the GPU: phong and extinction images and the brute-force
+    shadow oracle against the reference (float64 paths; only log1p/exp/pow's
+    last ulp can differ)."""
+    g = load_golden("extra_modes")
+    m = g["meta"]
+    for aniso in (False, True):
+        tag = "_aniso" if aniso else ""
+        data = g["volume_aniso"] if aniso else g["volume"]
+        v = sb.VolumeDataset.from_array(data, spacing=tuple(m["spacing_aniso"]) if aniso else (1.0, 1.0, 1.0))
+        tf = sb.preset(m["tf"])
+        cam = sb.Camera(position=m["cam_pos"], target=(0.5, 0.5, 0.5), fov_deg=m["fov"])
+        light = sb.Light(direction=m["light_dir"])
+        for mode in ("phong", "extinction"):
+            s = sb.RenderSettings(camera=cam, light=light, viewport=tuple(m["viewport"]), step=m["step"],
+                                  shading_mode=mode, ambient_floor=m["floor"], phong=sb.PhongParams(*m["phong"]))
+            st = parity_stats(sb.render(v, tf, s), g[f"image_{mode}{tag}"])
+            _report(f"extra {mode}{tag}", st)
+            assert st["max_abs"] <= 1e-6
+        got = sb.shadow_oracle_many(v, tf, g["probe"], light, m["oracle_step"])
+        want = g["oracle_aniso" if aniso else "oracle"]
+        assert np.abs(got - want).max() <= 1e-12

@@ -107,3 +107,33 @@ def test_case_render_bit_exact(case):
             continue  # ~7 s on one core; covered by the GPU test against the same golden
         img = O.render_image(v, tf.lut, settings_for(mode, lookup), buf)
         assert np.array_equal(img, g[f"image_{mode}_{lookup}"]), (case, mode, lookup)
+
+
+def _extra_scene(g, aniso=False):
+    from paper_2008_06134_b200 import scene
+    m = g["meta"]
+    data = g["volume_aniso"] if aniso else g["volume"]
+    v = scene.VolumeDataset.from_array(data, spacing=tuple(m["spacing_aniso"]) if aniso else (1.0, 1.0, 1.0))
+    tf = scene.preset(m["tf"])
+    cam = scene.Camera(position=m["cam_pos"], target=(0.5, 0.5, 0.5), fov_deg=m["fov"])
+    light = scene.Light(direction=m["light_dir"])
+
+    def settings(mode):
+        return scene.RenderSettings(camera=cam, light=light, viewport=tuple(m["viewport"]), step=m["step"],
+                                    shading_mode=mode, ambient_floor=m["floor"],
+                                    phong=scene.PhongParams(*m["phong"]))
+    return v, tf, light, settings
+
+
+def test_extra_modes_bit_exact():
+    """phong / extinction images, gradient and shadow_oracle_many vs the reference."""
+    g = load_golden("extra_modes")
+    for aniso in (False, True):
+        tag = "_aniso" if aniso else ""
+        v, tf, light, settings = _extra_scene(g, aniso)
+        for mode in ("phong", "extinction"):
+            assert np.array_equal(O.render_image(v, tf.lut, settings(mode)), g[f"image_{mode}{tag}"]), (mode, tag)
+        want = g["oracle_aniso" if aniso else "oracle"]
+        assert np.array_equal(O.shadow_oracle(v, tf.lut, g["probe"], light.direction, g["meta"]["oracle_step"]), want)
+    v, *_ = _extra_scene(g, True)
+    assert np.array_equal(O.gradient(v, g["probe"]), g["grad"])
