@@ -184,9 +184,11 @@ def test_errors_match_reference_types(sb):
                           light=sb.Light(direction=(0, 0, 1)), viewport=(8, 8), shading_mode="cone")
     with pytest.raises(sb.ConfigError):
         sb.render(v, tf, s)
-    with pytest.raises(ValueError):
+    with pytest.raises(ValueError):  # unknown lookup mode (lightbuffer.py:262-263)
         sb.render(v, tf, sb.RenderSettings(camera=s.camera, light=s.light, viewport=(8, 8),
-                                           shading_mode="phong"))
+                                           shading_mode="sbrc_shadow", lookup_mode="cubic"),
+                  sb.build_attenuation_buffer(v, tf, sb.LightCamera.fit((0, 0, 1), (1, 1, 1), (8, 8)),
+                                              sb.make_slice_stack((0, 0, 1), 4)))
 
 
 def test_sbrc_empty_buffer_equals_none(sb):
