@@ -67,8 +67,8 @@ def parse():
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--mode", default=None, help="override shading mode")
     ap.add_argument("--build", choices=("replicated", "sharded"), default="replicated")
-    ap.add_argument("--voxel", choices=("stored", "f64"), default="stored",
-                    help="device copy of a float32 volume: as stored, or widened to float64")
+    ap.add_argument("--voxel", choices=("linear", "octet"), default="linear",
+                    help="device layout of the volume: linear (x-fastest) or octets (8 corners per cell)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also print a per-kernel detail line to stderr")
@@ -344,8 +344,8 @@ def run_ours(a, cfg, mode):
     tf, cam, spec, settings = scene_objects(cfg, mode)
     t0 = time.perf_counter()
     dvol, host_vol = device_volume_for(cfg, dev)
-    if a.voxel == "f64" and dvol.voxel_type == 0:
-        dvol = dvol.widened()
+    if a.voxel == "octet":
+        dvol = dvol.octets()
     torch.cuda.synchronize()
     vol_gen_s = time.perf_counter() - t0
     fr = FrameRenderer(dvol, tf, cam, spec, settings, build=a.build if world > 1 else "replicated",
@@ -410,7 +410,7 @@ def run_ours(a, cfg, mode):
         e2e = e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev)
 
     # ---- roofline of the dominant kernel
-    vbytes = min(dvol.data.element_size(), 4)  # algorithmic V counts the stored source bytes
+    vbytes = {0: 4, 1: 1, 2: 2}[dvol.voxel_type % 4]  # algorithmic V counts the source bytes per voxel
     V, A, I = algorithmic_bytes(cfg, vbytes, world)
     k1_bytes = V + (A if (world == 1 or a.build == "replicated") else A // world)
     k2_bytes = (V + A + I // world) if mode != "none" else (V + I // world)

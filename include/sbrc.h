@@ -54,7 +54,11 @@ typedef enum sbrc_voxel_type {
   SBRC_VOXEL_F32 = 0, /* already-normalised float32 (volume.py:147-149)          */
   SBRC_VOXEL_U8 = 1,  /* raw u8, normalised at fetch as (float)x / 255.0f (volume.py:143-144) */
   SBRC_VOXEL_U16 = 2, /* raw u16, normalised at fetch as (float)x / 65535.0f (volume.py:145-146) */
-  SBRC_VOXEL_F64 = 3  /* float32 values widened to float64 at upload (no per-fetch conversion) */
+  /* octet layouts (sbrc_pack_octets): cell (cx,cy,cz) in [0,n]^3 stores the 8
+   * clamped corners of the trilinear cell with low corner (cx-1,cy-1,cz-1) */
+  SBRC_VOXEL_F32_OCT = 4,
+  SBRC_VOXEL_U8_OCT = 5,
+  SBRC_VOXEL_U16_OCT = 6
 } sbrc_voxel_type;
 
 typedef enum sbrc_shading {
@@ -165,6 +169,10 @@ int64_t sbrc_struct_size(int which); /* 0 volume, 1 light_frame, 2 build, 3 rend
  * u8/u16 stay raw and are normalised at fetch). Replaces load_raw's
  * normalisation (volume.py:141-151) for the device copy. */
 int sbrc_volume_check(const sbrc_volume* v);
+
+/* K0: repack a linear F32/U8/U16 volume into its octet layout; dst holds
+ * (nx+1)(ny+1)(nz+1) cells of 8 voxels (32/8/16 bytes). */
+int sbrc_pack_octets(const sbrc_volume* src, void* dst, void* stream);
 
 /* K1: attenuation build (lightbuffer.py:144-199). */
 int sbrc_build(const sbrc_build_params* p, void* stream);

@@ -21,13 +21,14 @@ MAX_SHELLS = 8
 MAX_ANGLES = 16
 
 OK, EINVAL, ECONFIG, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4
-VOXEL_F32, VOXEL_U8, VOXEL_U16, VOXEL_F64 = 0, 1, 2, 3
+VOXEL_F32, VOXEL_U8, VOXEL_U16 = 0, 1, 2
+VOXEL_OCT = 4  # + base type: F32_OCT 4, U8_OCT 5, U16_OCT 6
 SHADE = {"none": 0, "sbrc_shadow": 1, "shell": 2, "cone": 3, "phong": 4, "extinction": 5}
 LOOKUP = {"linear": 0, "nearest": 1}
 
 #: every symbol include/sbrc.h declares
 EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume_check",
-           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_shadow_oracle", "sbrc_local_rows")
+           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_pack_octets", "sbrc_shadow_oracle", "sbrc_local_rows")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -84,6 +85,7 @@ def _load() -> C.CDLL:
     lib.sbrc_build.argtypes = [C.POINTER(SbrcBuildParams), C.c_void_p]
     lib.sbrc_render.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p]
     lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    lib.sbrc_pack_octets.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p]
     lib.sbrc_shadow_oracle.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_double, C.c_void_p, C.c_void_p]
     lib.sbrc_pack_quads.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,

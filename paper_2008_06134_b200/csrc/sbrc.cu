@@ -32,6 +32,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
+// Compile-time variants (A/B'd in profiles/r01_notes.md).
+#ifndef SBRC_BUILD_UNROLL
+#define SBRC_BUILD_UNROLL 2  // slices whose gathers are in flight together in K1
+#endif
+#ifndef SBRC_BUILD_SHUFFLE
+#define SBRC_BUILD_SHUFFLE 1  // one 16-byte store per quad (warp shuffle for the x+1 neighbour)
+#endif
+
 namespace {
 
 // ---------------------------------------------------------------- float64
@@ -73,24 +83,58 @@ __device__ __forceinline__ FloorF floor_f(float x) {
 template <int VT> struct Voxel;
 template <> struct Voxel<SBRC_VOXEL_F32> {
   using T = float;
+  static constexpr bool oct = false;
   static __device__ __forceinline__ double cvt(float x, const float*) { return (double)x; }
-};
-template <> struct Voxel<SBRC_VOXEL_F64> {
-  using T = double;
-  static __device__ __forceinline__ double cvt(double x, const float*) { return x; }
 };
 template <> struct Voxel<SBRC_VOXEL_U8> {
   using T = unsigned char;
+  static constexpr bool oct = false;
   static __device__ __forceinline__ double cvt(unsigned char x, const float* tab) {
     return reinterpret_cast<const double*>(tab)[x];
   }
 };
 template <> struct Voxel<SBRC_VOXEL_U16> {
   using T = unsigned short;
+  static constexpr bool oct = false;
   static __device__ __forceinline__ double cvt(unsigned short x, const float*) {
     return (double)__double2float_rn(dmul((double)x, 1.0 / 65535.0));
   }
 };
+// Octet layouts: cell (cx, cy, cz) in [0, n]^3 holds the 8 corner values of
+// the trilinear cell whose low corner is (cx-1, cy-1, cz-1), with the
+// reference's clamping i0 = clip(lo), i1 = clip(lo+1) baked in, ordered
+// d000 d100 d010 d110 d001 d101 d011 d111: one cell = one or two 16-byte loads.
+template <int BASE> struct OctetOf : Voxel<BASE> {
+  static constexpr bool oct = true;
+  static constexpr int base = BASE;
+};
+template <> struct Voxel<SBRC_VOXEL_F32_OCT> : OctetOf<SBRC_VOXEL_F32> {};
+template <> struct Voxel<SBRC_VOXEL_U8_OCT> : OctetOf<SBRC_VOXEL_U8> {};
+template <> struct Voxel<SBRC_VOXEL_U16_OCT> : OctetOf<SBRC_VOXEL_U16> {};
+
+template <typename T>
+__device__ __forceinline__ void load_octet(const void* data, unsigned cell, T r[8]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4* o = reinterpret_cast<const float4*>(data) + 2 * (size_t)cell;
+    const float4 a = __ldg(o), b = __ldg(o + 1);
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+  } else if constexpr (sizeof(T) == 2) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(data) + cell);
+    const unsigned w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      r[2 * i] = (T)(w[i] & 0xffffu);
+      r[2 * i + 1] = (T)(w[i] >> 16);
+    }
+  } else {
+    const uint2 a = __ldg(reinterpret_cast<const uint2*>(data) + cell);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      r[i] = (T)((a.x >> (8 * i)) & 0xffu);
+      r[4 + i] = (T)((a.y >> (8 * i)) & 0xffu);
+    }
+  }
+}
 
 // Cell-centred trilinear reconstruction, clamp-to-edge, 0 outside the unit
 // cube: sample_trilinear_many (volume.py:161-194), same op order. Split in
@@ -121,6 +165,13 @@ __device__ __forceinline__ void cell_fetch(const sbrc_volume& v, double px, doub
     cl.f[c] = dsub(g, fl.f);
     lo[c] = fl.i;
   }
+  if constexpr (Voxel<VT>::oct) {
+    // lo in [-1, n-1] (local in [0,1]); the octet grid is (n+1)^3
+    const unsigned cell = (unsigned)(lo[0] + 1) +
+                          (unsigned)(v.nx + 1) * ((unsigned)(lo[1] + 1) + (unsigned)(v.ny + 1) * (unsigned)(lo[2] + 1));
+    load_octet<T>(v.data, cell, cl.r);
+    return;
+  } else {
   const T* base = reinterpret_cast<const T*>(v.data);
   const unsigned nx = (unsigned)v.nx, nxy = (unsigned)v.nx * (unsigned)v.ny;
   if ((unsigned)lo[0] < (unsigned)(v.nx - 1) && (unsigned)lo[1] < (unsigned)(v.ny - 1) &&
@@ -145,6 +196,7 @@ __device__ __forceinline__ void cell_fetch(const sbrc_volume& v, double px, doub
     cl.r[2] = __ldg(base + (z0 + y1 + a[0])); cl.r[3] = __ldg(base + (z0 + y1 + b[0]));
     cl.r[4] = __ldg(base + (z1 + y0 + a[0])); cl.r[5] = __ldg(base + (z1 + y0 + b[0]));
     cl.r[6] = __ldg(base + (z1 + y1 + a[0])); cl.r[7] = __ldg(base + (z1 + y1 + b[0]));
+  }
   }
 }
 
@@ -219,13 +271,24 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   __shared__ double u8tab[256];
   for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x * blockDim.y)
     lut[i] = P.alpha_lut[i];
-  if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
+  if (std::is_same<typename Voxel<VT>::T, unsigned char>::value) fill_u8_table(u8tab);
   __syncthreads();
 
   const sbrc_light_frame& L = P.light;
+#if SBRC_BUILD_SHUFFLE
+  // Warps are 32 consecutive texels of one row overlapping the next warp by
+  // one: lane 31 only hands its layer pair to lane 30, so every quad is one
+  // 16-byte store (the right neighbour's pair arrives by shuffle).
+  const int lane = threadIdx.x;
+  const int x = blockIdx.x * 31 + lane;
+  const int y = P.row_begin + blockIdx.y * blockDim.y + threadIdx.y;
+  if (y >= P.row_end) return;  // whole warp (warps are rows)
+  const bool owner = lane < 31 && x < L.width;
+#else
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = P.row_begin + blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= L.width || y >= P.row_end) return;
+#endif
 
   // Texel centre in world (u, v) plane coordinates (_texel_world_grid, :134-141):
   // u0 + (i + 0.5) / W * (u1 - u0).
@@ -244,6 +307,18 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   const float* tab = reinterpret_cast<const float*>(u8tab);
   double T = 1.0;
   float prev = 0.0f;
+#if SBRC_BUILD_SHUFFLE
+  auto emit = [&](float4* layer_row, float a, float b) {
+    float ra = __shfl_down_sync(0xffffffffu, a, 1), rb = __shfl_down_sync(0xffffffffu, b, 1);
+    if (x == L.width - 1) {
+      ra = a;
+      rb = b;
+    }
+    if (owner) layer_row[x] = make_float4(a, b, ra, rb);
+  };
+#else
+  auto emit = [&](float4* layer_row, float a, float b) { emit_pair(layer_row, x, L.width, a, b); };
+#endif
   // One slice of the recurrence: stored = T (:169); if covered, alpha from the
   // cell, optional compensation (:193-196), T *= 1 - alpha (:197-198).
   auto step_slice = [&](bool covered, const Cell<VT>& cl) -> float {
@@ -264,33 +339,38 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
     pz = dadd(base[2], dmul(off, L.light_dir[2]));
   };
   int k = 0;
-  // Slices in pairs: the gathers of both are issued before either is combined
-  // (the product order of T is unchanged, so the result stays bit-exact).
-  for (; k + 1 < L.n_slices; k += 2) {
-    double ax, ay, az, bx, by, bz;
-    point(k, ax, ay, az);
-    point(k + 1, bx, by, bz);
-    const bool ca = in_cube(ax, ay, az), cb = in_cube(bx, by, bz);
-    Cell<VT> la, lb;
-    if (ca) cell_fetch<VT, UNIT>(P.volume, ax, ay, az, la);
-    if (cb) cell_fetch<VT, UNIT>(P.volume, bx, by, bz, lb);
-    const float sa = step_slice(ca, la);
-    const float sb = step_slice(cb, lb);
-    if (k > 0) emit_pair(row + (size_t)(k - 1) * ks, x, L.width, prev, sa);
-    emit_pair(row + (size_t)k * ks, x, L.width, sa, sb);
-    prev = sb;
+  // SBRC_BUILD_UNROLL slices at a time: the gathers of all of them are issued
+  // before any is combined (the product order of T is unchanged, so the
+  // result stays bit-exact).
+  constexpr int U = SBRC_BUILD_UNROLL;
+  for (; k + U <= L.n_slices; k += U) {
+    bool cov[U];
+    Cell<VT> cl[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double px, py, pz;
+      point(k + u, px, py, pz);
+      cov[u] = in_cube(px, py, pz);
+      if (cov[u]) cell_fetch<VT, UNIT>(P.volume, px, py, pz, cl[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float st = step_slice(cov[u], cl[u]);
+      if (k + u > 0) emit(row + (size_t)(k + u - 1) * ks, prev, st);
+      prev = st;
+    }
   }
-  if (k < L.n_slices) {
+  for (; k < L.n_slices; ++k) {
     double ax, ay, az;
     point(k, ax, ay, az);
     const bool ca = in_cube(ax, ay, az);
     Cell<VT> la;
     if (ca) cell_fetch<VT, UNIT>(P.volume, ax, ay, az, la);
     const float sa = step_slice(ca, la);
-    if (k > 0) emit_pair(row + (size_t)(k - 1) * ks, x, L.width, prev, sa);
+    if (k > 0) emit(row + (size_t)(k - 1) * ks, prev, sa);
     prev = sa;
   }
-  emit_pair(row + (size_t)(L.n_slices - 1) * ks, x, L.width, prev, prev);
+  emit(row + (size_t)(L.n_slices - 1) * ks, prev, prev);
 }
 
 // Repack a plain stack into quads (one thread per texel, loop over layers).
@@ -486,7 +566,7 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
     lut[i] = reinterpret_cast<const double2*>(P.lut_rgba)[i];
   if (SHADING == SBRC_SHADE_EXTINCTION)
     for (int i = threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x) alut[i] = P.lut_rgba[4 * i + 3];
-  if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
+  if (std::is_same<typename Voxel<VT>::T, unsigned char>::value) fill_u8_table(u8tab);
 
   const sbrc_light_frame& LF = P.light;
   // Light space (world_to_light_uv_many :202-212, slice_index_many slicing.py:101-105):
@@ -853,7 +933,7 @@ __global__ void __launch_bounds__(256) shadow_oracle_kernel(const sbrc_volume V,
   __shared__ double alut[SBRC_LUT_SIZE];
   __shared__ double u8tab[256];
   for (int i = threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x) alut[i] = alpha_lut[i];
-  if (VT == SBRC_VOXEL_U8) fill_u8_table(u8tab);
+  if (std::is_same<typename Voxel<VT>::T, unsigned char>::value) fill_u8_table(u8tab);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
@@ -862,12 +942,35 @@ __global__ void __launch_bounds__(256) shadow_oracle_kernel(const sbrc_volume V,
   out[i] = light_march<VT, UNIT, false>(V, alut, reinterpret_cast<const float*>(u8tab), p, tl, step);
 }
 
+// K0 octet repack: one thread per octet cell (cx, cy, cz) in [0, n]^3.
+template <typename T>
+__global__ void __launch_bounds__(256) pack_octets_kernel(const T* __restrict__ src, int nx, int ny, int nz, T* dst) {
+  const long long cells = (long long)(nx + 1) * (ny + 1) * (nz + 1);
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int cx = (int)(c % (nx + 1));
+    const int cy = (int)((c / (nx + 1)) % (ny + 1));
+    const int cz = (int)(c / ((long long)(nx + 1) * (ny + 1)));
+    const int x0 = max(cx - 1, 0), x1 = min(cx, nx - 1);
+    const int y0 = max(cy - 1, 0), y1 = min(cy, ny - 1);
+    const int z0 = max(cz - 1, 0), z1 = min(cz, nz - 1);
+    const size_t sy = (size_t)nx, sz = (size_t)nx * ny;
+    T* o = dst + 8 * (size_t)c;
+    o[0] = src[z0 * sz + y0 * sy + x0]; o[1] = src[z0 * sz + y0 * sy + x1];
+    o[2] = src[z0 * sz + y1 * sy + x0]; o[3] = src[z0 * sz + y1 * sy + x1];
+    o[4] = src[z1 * sz + y0 * sy + x0]; o[5] = src[z1 * sz + y0 * sy + x1];
+    o[6] = src[z1 * sz + y1 * sy + x0]; o[7] = src[z1 * sz + y1 * sy + x1];
+  }
+}
+
 // ---------------------------------------------------------------- dispatch
 bool volume_ok(const sbrc_volume& v) {
   if (v.data == nullptr) return false;
   if (v.nx < 2 || v.ny < 2 || v.nz < 2) return false;  // volume.py:80-81
   if ((unsigned long long)v.nx * v.ny * v.nz >= (1ull << 32)) return false;  // 32-bit voxel offsets
-  if (v.voxel_type < SBRC_VOXEL_F32 || v.voxel_type > SBRC_VOXEL_F64) return false;
+  if (v.voxel_type < SBRC_VOXEL_F32 || v.voxel_type > SBRC_VOXEL_U16_OCT) return false;
+  if (v.voxel_type >= SBRC_VOXEL_F32_OCT && (unsigned long long)(v.nx + 1) * (v.ny + 1) * (v.nz + 1) >= (1ull << 32))
+    return false;
   for (int c = 0; c < 3; ++c)
     if (!(v.box_ext[c] > 0.0)) return false;
   return true;
@@ -894,7 +997,11 @@ bool unit_box(const sbrc_volume& v) {
 template <int VT>
 void launch_build(const sbrc_build_params& p, cudaStream_t s) {
   dim3 block(32, 8);
+#if SBRC_BUILD_SHUFFLE
+  dim3 grid((p.light.width + 30) / 31, (p.row_end - p.row_begin + 7) / 8);
+#else
   dim3 grid((p.light.width + 31) / 32, (p.row_end - p.row_begin + 7) / 8);
+#endif
   if (unit_box(p.volume)) build_kernel<VT, true><<<grid, block, 0, s>>>(p);
   else build_kernel<VT, false><<<grid, block, 0, s>>>(p);
 }
@@ -929,9 +1036,11 @@ template <int SH, int LK>
 void launch_march_vt(const sbrc_render_params& p, cudaStream_t s) {
   switch (p.volume.voxel_type) {
     case SBRC_VOXEL_F32: launch_march_box<SH, LK, SBRC_VOXEL_F32>(p, s); break;
-    case SBRC_VOXEL_F64: launch_march_box<SH, LK, SBRC_VOXEL_F64>(p, s); break;
     case SBRC_VOXEL_U8: launch_march_box<SH, LK, SBRC_VOXEL_U8>(p, s); break;
-    default: launch_march_box<SH, LK, SBRC_VOXEL_U16>(p, s); break;
+    case SBRC_VOXEL_U16: launch_march_box<SH, LK, SBRC_VOXEL_U16>(p, s); break;
+    case SBRC_VOXEL_F32_OCT: launch_march_box<SH, LK, SBRC_VOXEL_F32_OCT>(p, s); break;
+    case SBRC_VOXEL_U8_OCT: launch_march_box<SH, LK, SBRC_VOXEL_U8_OCT>(p, s); break;
+    default: launch_march_box<SH, LK, SBRC_VOXEL_U16_OCT>(p, s); break;
   }
 }
 template <int SH>
@@ -986,9 +1095,11 @@ int sbrc_build(const sbrc_build_params* p, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (p->volume.voxel_type) {
     case SBRC_VOXEL_F32: launch_build<SBRC_VOXEL_F32>(*p, s); break;
-    case SBRC_VOXEL_F64: launch_build<SBRC_VOXEL_F64>(*p, s); break;
     case SBRC_VOXEL_U8: launch_build<SBRC_VOXEL_U8>(*p, s); break;
-    default: launch_build<SBRC_VOXEL_U16>(*p, s); break;
+    case SBRC_VOXEL_U16: launch_build<SBRC_VOXEL_U16>(*p, s); break;
+    case SBRC_VOXEL_F32_OCT: launch_build<SBRC_VOXEL_F32_OCT>(*p, s); break;
+    case SBRC_VOXEL_U8_OCT: launch_build<SBRC_VOXEL_U8_OCT>(*p, s); break;
+    default: launch_build<SBRC_VOXEL_U16_OCT>(*p, s); break;
   }
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
@@ -1003,6 +1114,30 @@ int sbrc_pack_quads(const float* plain, int64_t plain_layer_stride, int64_t plai
   dim3 grid((width + 31) / 32, (height + 7) / 8);
   pack_quads_kernel<<<grid, block, 0, s>>>(plain, plain_layer_stride, plain_row_stride, n, height, width, quads,
                                            quad_layer_stride, quad_row_stride);
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_pack_octets(const sbrc_volume* src, void* dst, void* stream) {
+  if (src == nullptr || dst == nullptr || !volume_ok(*src) || src->voxel_type > SBRC_VOXEL_U16) return SBRC_EINVAL;
+  if ((unsigned long long)(src->nx + 1) * (src->ny + 1) * (src->nz + 1) >= (1ull << 32)) return SBRC_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int blocks = 148 * 16;
+  switch (src->voxel_type) {
+    case SBRC_VOXEL_F32:
+      pack_octets_kernel<float><<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(src->data), src->nx, src->ny,
+                                                       src->nz, reinterpret_cast<float*>(dst));
+      break;
+    case SBRC_VOXEL_U8:
+      pack_octets_kernel<unsigned char><<<blocks, 256, 0, s>>>(reinterpret_cast<const unsigned char*>(src->data),
+                                                               src->nx, src->ny, src->nz,
+                                                               reinterpret_cast<unsigned char*>(dst));
+      break;
+    default:
+      pack_octets_kernel<unsigned short><<<blocks, 256, 0, s>>>(reinterpret_cast<const unsigned short*>(src->data),
+                                                                src->nx, src->ny, src->nz,
+                                                                reinterpret_cast<unsigned short*>(dst));
+      break;
+  }
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 
@@ -1022,9 +1157,11 @@ int sbrc_shadow_oracle(const sbrc_volume* v, const double* alpha_lut, const doub
                                                                  to_light[2], step, out))
   switch (v->voxel_type) {
     case SBRC_VOXEL_F32: SBRC_ORACLE(SBRC_VOXEL_F32); break;
-    case SBRC_VOXEL_F64: SBRC_ORACLE(SBRC_VOXEL_F64); break;
     case SBRC_VOXEL_U8: SBRC_ORACLE(SBRC_VOXEL_U8); break;
-    default: SBRC_ORACLE(SBRC_VOXEL_U16); break;
+    case SBRC_VOXEL_U16: SBRC_ORACLE(SBRC_VOXEL_U16); break;
+    case SBRC_VOXEL_F32_OCT: SBRC_ORACLE(SBRC_VOXEL_F32_OCT); break;
+    case SBRC_VOXEL_U8_OCT: SBRC_ORACLE(SBRC_VOXEL_U8_OCT); break;
+    default: SBRC_ORACLE(SBRC_VOXEL_U16_OCT); break;
   }
 #undef SBRC_ORACLE
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
