@@ -186,6 +186,16 @@ int sbrc_pack_quads(const float* plain, int64_t plain_layer_stride, int64_t plai
                     int n, int height, int width, float* quads, int64_t quad_layer_stride,
                     int64_t quad_row_stride, void* stream);
 
+/* Light factor at m float64 world points pts[3*i..] for shading sbrc_shadow /
+ * shell / cone (p->shading, p->lookup, kernels, light frame, quads, light
+ * colour, ambient floor; the image/volume fields are ignored): out[4*i..] =
+ * (scalar, factor_r, factor_g, factor_b) = lookup_light_scalar_many /
+ * _shell_scalar / _cone_scalar (lightbuffer.py:256-287, raycaster.py:239-300)
+ * followed by _factor_from_intensity (raycaster.py:197-201). eye (3 doubles)
+ * orients the cone ring (shade_cone's eye); NULL = the plane_basis fallback. */
+int sbrc_light_factor(const sbrc_render_params* p, const double* pts, int64_t m, const double* eye, float* out,
+                      void* stream);
+
 /* GPU shadow_oracle_many (raycaster.py:335-366): transmittance from each of
  * m float64 points pts[3*i..] toward the light, a straight march with
  * step-corrected opacity: out[i] = prod (1 - min(a, 1 - 1e-6)).

@@ -29,5 +29,15 @@ from .scene import (  # noqa: F401
     preset,
 )
 from .lightbuffer import AttenuationBuffer, build_attenuation_buffer  # noqa: F401
-from .raycaster import render, render_device, shadow_oracle_many  # noqa: F401
+from .raycaster import (  # noqa: F401
+    lookup_light,
+    lookup_light_many,
+    lookup_light_scalar_many,
+    render,
+    render_device,
+    shade_cone,
+    shade_sbrc_shadow,
+    shade_shell,
+    shadow_oracle_many,
+)
 from .device import DeviceVolume, device_volume  # noqa: F401

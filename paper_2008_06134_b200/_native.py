@@ -28,7 +28,8 @@ LOOKUP = {"linear": 0, "nearest": 1}
 
 #: every symbol include/sbrc.h declares
 EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume_check",
-           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_pack_octets", "sbrc_shadow_oracle", "sbrc_local_rows")
+           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_pack_octets", "sbrc_shadow_oracle", "sbrc_light_factor",
+           "sbrc_local_rows")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -85,6 +86,8 @@ def _load() -> C.CDLL:
     lib.sbrc_build.argtypes = [C.POINTER(SbrcBuildParams), C.c_void_p]
     lib.sbrc_render.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p]
     lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    lib.sbrc_light_factor.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]
     lib.sbrc_pack_octets.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p]
     lib.sbrc_shadow_oracle.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_double, C.c_void_p, C.c_void_p]

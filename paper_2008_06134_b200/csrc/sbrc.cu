@@ -963,6 +963,99 @@ __global__ void __launch_bounds__(256) pack_octets_kernel(const T* __restrict__ 
   }
 }
 
+// Light factor at arbitrary world points: lookup_light_scalar_many
+// (lightbuffer.py:256-287), _shell_scalar (raycaster.py:239-250) and
+// _cone_scalar (:266-300) with the cone basis from `eye - p` per point (or the
+// plane_basis fallback when eye is absent), then _factor_from_intensity
+// (:197-201). Same device lookup code as K2 (general path); out[i] =
+// (scalar, factor_r, factor_g, factor_b).
+template <int LOOKUP>
+__global__ void __launch_bounds__(256) light_factor_kernel(const sbrc_render_params P, const double* __restrict__ pts,
+                                                           int64_t m, int has_eye, double ex, double ey, double ez,
+                                                           float4* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const sbrc_light_frame& LF = P.light;
+  const double sx = (double)LF.width / (LF.u_range[1] - LF.u_range[0]);
+  const double sy = (double)LF.height / (LF.v_range[1] - LF.v_range[0]);
+  const double si = (double)LF.n_slices / (LF.d_max - LF.d_min);
+  QuadTex tex;
+  tex.q = reinterpret_cast<const float4*>(P.quads);
+  tex.qk = (unsigned)P.quad_layer_stride;
+  tex.qy = (unsigned)P.quad_row_stride;
+  tex.qy1 = LF.height > 1 ? tex.qy : 0u;
+  tex.txmax = (float)LF.width - 0.5f;
+  tex.tymax = (float)LF.height - 0.5f;
+  tex.xa_max = (float)max(LF.width - 2, 0);
+  tex.ya_max = (float)max(LF.height - 2, 0);
+  tex.li_max = (float)(LF.n_slices - 1);
+  tex.ka_max = (float)max(LF.n_slices - 2, 0);
+  const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+  double pu = 0, pv = 0, pl = 0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    pu += p[c] * LF.axis_u[c];
+    pv += p[c] * LF.axis_v[c];
+    pl += p[c] * LF.light_dir[c];
+  }
+  const float tx = (float)((pu - LF.u_range[0]) * sx - 0.5);
+  const float ty = (float)((pv - LF.v_range[0]) * sy - 0.5);
+  const float li = (float)((pl - LF.d_min) * si - (LOOKUP == SBRC_LOOKUP_NEAREST ? 0.0 : 0.5));
+  float scalar;
+  if (P.shading == SBRC_SHADE_SHADOW) {
+    scalar = light_lookup<LOOKUP>(tex, tx, ty, li);
+  } else if (P.shading == SBRC_SHADE_SHELL) {
+    float acc = 0.0f;
+    for (int sh = 0; sh < P.shell_count; ++sh) {
+      const double r = P.shell_radius[sh];
+      float shell = 0.0f;
+      for (int a = 0; a < 3; ++a) {
+        const float du = (float)(r * LF.axis_u[a] * sx), dv = (float)(r * LF.axis_v[a] * sy);
+        const float dl = (float)(r * LF.light_dir[a] * si);
+        shell += light_lookup<LOOKUP>(tex, tx + du, ty + dv, li + dl);
+        shell += light_lookup<LOOKUP>(tex, tx - du, ty - dv, li - dl);
+      }
+      acc += (float)P.shell_weight[sh] * shell / 6.0f;
+    }
+    scalar = acc;
+  } else {  // cone
+    float bu = 1.0f, bv = 0.0f;  // plane_basis(L)[0] = axis_u
+    if (has_eye) {
+      const double e[3] = {ex - p[0], ey - p[1], ez - p[2]};
+      const double el = e[0] * LF.light_dir[0] + e[1] * LF.light_dir[1] + e[2] * LF.light_dir[2];
+      double b[3], nb = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        b[c] = e[c] - el * LF.light_dir[c];
+        nb += b[c] * b[c];
+      }
+      nb = sqrt(nb);
+      if (nb > 1e-12) {
+        bu = (float)((b[0] * LF.axis_u[0] + b[1] * LF.axis_u[1] + b[2] * LF.axis_u[2]) / nb);
+        bv = (float)((b[0] * LF.axis_v[0] + b[1] * LF.axis_v[1] + b[2] * LF.axis_v[2]) / nb);
+      }
+    }
+    const double spacing = (LF.d_max - LF.d_min) / LF.n_slices;
+    float acc = 0.0f;
+    for (int a = 1; a <= P.cone_axis_samples; ++a) {
+      const double r = P.cone_ring * a * spacing;
+      for (int j = 0; j < P.cone_angle_count; ++j) {
+        const double c = P.cone_cos[j], sn = P.cone_sin[j];
+        const float ox = (float)(r * sx * (bu * c - bv * sn)), oy = (float)(r * sy * (bv * c + bu * sn));
+        acc += light_lookup<LOOKUP>(tex, tx + ox, ty + oy, li - (float)a);
+      }
+    }
+    scalar = acc / (float)(P.cone_axis_samples * P.cone_angle_count);
+  }
+  float f[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float col = P.light_color[c];
+    f[c] = col > 0.f ? fmaxf(scalar * col, P.ambient_floor) / col : 1.0f;
+  }
+  out[i] = make_float4(scalar, f[0], f[1], f[2]);
+}
+
 // ---------------------------------------------------------------- dispatch
 bool volume_ok(const sbrc_volume& v) {
   if (v.data == nullptr) return false;
@@ -1138,6 +1231,29 @@ int sbrc_pack_octets(const sbrc_volume* src, void* dst, void* stream) {
                                                                 reinterpret_cast<unsigned short*>(dst));
       break;
   }
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_light_factor(const sbrc_render_params* p, const double* pts, int64_t m, const double* eye, float* out,
+                      void* stream) {
+  if (p == nullptr || out == nullptr || m < 0 || (m > 0 && pts == nullptr)) return SBRC_EINVAL;
+  if (p->shading < SBRC_SHADE_SHADOW || p->shading > SBRC_SHADE_CONE) return SBRC_EINVAL;
+  if (p->lookup != SBRC_LOOKUP_LINEAR && p->lookup != SBRC_LOOKUP_NEAREST) return SBRC_EINVAL;
+  if (p->quads == nullptr) return SBRC_ECONFIG;
+  if (!light_ok(p->light) || !quads_ok(p->light, p->quad_layer_stride, p->quad_row_stride)) return SBRC_EINVAL;
+  if (p->shading == SBRC_SHADE_SHELL && (p->shell_count < 1 || p->shell_count > SBRC_MAX_SHELLS)) return SBRC_EINVAL;
+  if (p->shading == SBRC_SHADE_CONE && (p->cone_axis_samples < 1 || p->cone_angle_count < 1 ||
+                                        p->cone_angle_count > SBRC_MAX_ANGLES))
+    return SBRC_EINVAL;
+  if (m == 0) return SBRC_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned blocks = (unsigned)((m + 255) / 256);
+  const int he = eye != nullptr;
+  const double ex = he ? eye[0] : 0.0, ey = he ? eye[1] : 0.0, ez = he ? eye[2] : 0.0;
+  if (p->lookup == SBRC_LOOKUP_NEAREST)
+    light_factor_kernel<SBRC_LOOKUP_NEAREST><<<blocks, 256, 0, s>>>(*p, pts, m, he, ex, ey, ez, reinterpret_cast<float4*>(out));
+  else
+    light_factor_kernel<SBRC_LOOKUP_LINEAR><<<blocks, 256, 0, s>>>(*p, pts, m, he, ex, ey, ez, reinterpret_cast<float4*>(out));
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 

@@ -18,12 +18,14 @@ measured against (raycaster.py:356-366).
 from __future__ import annotations
 
 import ctypes as C
+import math
 
 import numpy as np
 import torch
 
 from . import _native as N
-from .device import _require_cuda, current_stream_handle, device_volume, f64_tensor, pack_quads, render_params, to_host
+from .device import (_require_cuda, current_stream_handle, device_volume, f64_tensor, light_frame, pack_quads,
+                     quad_strides, render_params, to_host)
 from .lightbuffer import AttenuationBuffer
 from .scene import BUFFER_MODES, ConfigError
 
@@ -94,3 +96,78 @@ def shadow_oracle_many(v, tf, pts, light, oracle_step: float, *, device=None) ->
                                      float(oracle_step), out.data_ptr(), current_stream_handle()),
             "sbrc_shadow_oracle")
     return to_host(out).reshape(np.asarray(pts).shape[:-1])
+
+
+# ------------------------------------------------------------ point-wise light API
+def _light_factor(buffer, pts, shading: str, lookup: str = "linear", *, shell_kernel=None, cone_kernel=None,
+                  eye=None, ambient_floor: float = 0.0, device=None) -> np.ndarray:
+    """(M, 4) float32 numpy: (scalar, factor_r, factor_g, factor_b) at world points."""
+    if lookup not in N.LOOKUP:
+        raise ValueError(f"unknown lookup mode {lookup!r}")
+    dev = _require_cuda(device)
+    quads = _quads_of(buffer, dev)
+    cam, spec = buffer.camera, buffer.spec
+    p = N.SbrcRenderParams()
+    p.shading, p.lookup = N.SHADE[shading], N.LOOKUP[lookup]
+    p.light = light_frame(cam, spec, None)
+    p.quads = quads.data_ptr()
+    p.quad_layer_stride, p.quad_row_stride = quad_strides(quads)
+    p.light_color[:] = [float(c) for c in np.asarray(cam.light_color, dtype=np.float64)]
+    p.ambient_floor = float(ambient_floor)
+    if shading == "shell":
+        if len(shell_kernel.radii) > N.MAX_SHELLS:
+            raise ValueError(f"at most {N.MAX_SHELLS} shells")
+        p.shell_count = len(shell_kernel.radii)
+        for i, (r, w) in enumerate(zip(shell_kernel.radii, shell_kernel.weights)):
+            p.shell_radius[i], p.shell_weight[i] = float(r), float(w)
+    if shading == "cone":
+        if not 1 <= len(cone_kernel.angles) <= N.MAX_ANGLES:
+            raise ValueError(f"cone kernel must have 1..{N.MAX_ANGLES} angles")
+        p.cone_axis_samples, p.cone_angle_count = int(cone_kernel.axis_samples), len(cone_kernel.angles)
+        p.cone_ring = float(cone_kernel.ring_radius_per_step)
+        for i, th in enumerate(cone_kernel.angles):
+            p.cone_cos[i], p.cone_sin[i] = math.cos(th), math.sin(th)
+    q = np.ascontiguousarray(np.asarray(pts, dtype=np.float64).reshape(-1, 3))
+    out = torch.empty((q.shape[0], 4), dtype=torch.float32, device=dev)
+    if q.shape[0]:
+        pd = f64_tensor(q, dev)
+        e = None if eye is None else (C.c_double * 3)(*[float(x) for x in np.asarray(eye, dtype=np.float64)])
+        N.check(N.lib.sbrc_light_factor(C.byref(p), pd.data_ptr(), q.shape[0], e, out.data_ptr(),
+                                        current_stream_handle()), "sbrc_light_factor")
+    return to_host(out)
+
+
+def lookup_light_scalar_many(b, pts, mode: str = "linear") -> np.ndarray:
+    """GPU lookup_light_scalar_many (lightbuffer.py:256-287); float64 numpy of pts' shape[:-1]."""
+    pts = np.asarray(pts, dtype=np.float64)
+    return _light_factor(b, pts, "sbrc_shadow", mode)[:, 0].astype(np.float64).reshape(pts.shape[:-1])
+
+
+def lookup_light_many(b, pts, mode: str = "linear") -> np.ndarray:
+    """rgb light arriving at world points (lightbuffer.py:290-293)."""
+    return lookup_light_scalar_many(b, pts, mode)[..., None] * np.asarray(b.camera.light_color)
+
+
+def lookup_light(b, p_world, mode: str = "linear") -> np.ndarray:
+    return lookup_light_many(b, np.asarray(p_world, dtype=np.float64)[None, :], mode)[0]
+
+
+def shade_sbrc_shadow(sample_p, buffer, ambient_floor: float = 0.0, mode: str = "linear") -> np.ndarray:
+    """Volume-shadow factor at one point (raycaster.py:231-236)."""
+    f = _light_factor(buffer, np.asarray(sample_p, dtype=np.float64)[None, :], "sbrc_shadow", mode,
+                      ambient_floor=ambient_floor)
+    return f[0, 1:].astype(np.float64)
+
+
+def shade_shell(sample_p, buffer, kernel, ambient_floor: float = 0.0, mode: str = "linear") -> np.ndarray:
+    """Shell scattering factor at one point (raycaster.py:253-258)."""
+    f = _light_factor(buffer, np.asarray(sample_p, dtype=np.float64)[None, :], "shell", mode, shell_kernel=kernel,
+                      ambient_floor=ambient_floor)
+    return f[0, 1:].astype(np.float64)
+
+
+def shade_cone(sample_p, buffer, kernel, eye=None, ambient_floor: float = 0.0, mode: str = "linear") -> np.ndarray:
+    """Cone scattering factor at one point (raycaster.py:303-309)."""
+    f = _light_factor(buffer, np.asarray(sample_p, dtype=np.float64)[None, :], "cone", mode, cone_kernel=kernel,
+                      eye=eye, ambient_floor=ambient_floor)
+    return f[0, 1:].astype(np.float64)
