@@ -163,12 +163,17 @@ int sbrc_abi_version(void);
 const char* sbrc_strerror(int status);
 
 /* sizeof() of the params structs, so a binding can verify its layout. */
-int64_t sbrc_struct_size(int which); /* 0 volume, 1 light_frame, 2 build, 3 render */
+int64_t sbrc_struct_size(int which); /* 0 volume, 1 light_frame, 2 build, 3 render, 4 half_angle */
 
 /* K0: repack a raw voxel stream already on the device (no-op copy for f32;
  * u8/u16 stay raw and are normalised at fetch). Replaces load_raw's
  * normalisation (volume.py:141-151) for the device copy. */
 int sbrc_volume_check(const sbrc_volume* v);
+
+/* K0: load_raw's float32 min-max normalisation in place (volume.py:147-151):
+ * data[i] = fl32(fl32(data[i] - lo) / range), range = fl32(hi - lo) > 0 —
+ * numpy's float32 arithmetic, so bit-identical. */
+int sbrc_normalize_f32(float* data, int64_t n, float lo, float range, void* stream);
 
 /* K0: repack a linear F32/U8/U16 volume into its octet layout; dst holds
  * (nx+1)(ny+1)(nz+1) cells of 8 voxels (32/8/16 bytes). */
@@ -202,6 +207,36 @@ int sbrc_light_factor(const sbrc_render_params* p, const double* pts, int64_t m,
  * alpha_lut = tf.resolve(oracle_step)[:, 3]; to_light = -light.direction. */
 int sbrc_shadow_oracle(const sbrc_volume* v, const double* alpha_lut, const double* pts, int64_t m,
                        const double* to_light, double step, double* out, void* stream);
+
+/* Half-angle slicing baseline (halfangle.py:48-142): n slices perpendicular
+ * to the half vector; per slice an eye pass (composite into the float64
+ * accumulation image, modulated by the running light transmittance) and a
+ * light pass (attenuate it). pass_count = 2n. The host computes the
+ * per-frame scalars with numpy exactly as the reference does. */
+typedef struct sbrc_half_angle_params {
+  sbrc_volume volume;
+  const double* lut;          /* device 256x4 float64: the raw TransferFunction.lut */
+  const double* plane_offsets;/* device n float64: make_slice_stack(half, n).plane_offsets */
+  int32_t width, height;      /* viewport */
+  int32_t light_width, light_height;
+  int32_t n_slices;
+  int32_t front_to_back;      /* 1: "front_to_back", 0: "back_to_front" (_half_vector) */
+  double eye[3], forward[3], right[3], up2[3];
+  double tan_half, aspect;
+  double half[3];             /* half vector */
+  double delta;               /* stack.spacing */
+  double light_dir[3], axis_u[3], axis_v[3];
+  double u_range[2], v_range[2];
+  double hl, h_dot_u, h_dot_v, h_dot_e;
+  double* eye_accum;          /* device scratch H*W*4 float64 */
+  double* light_accum;        /* device scratch Hl*Wl float64 */
+  float* image;               /* device out (H, W, 4) float32 */
+} sbrc_half_angle_params;
+
+/* Runs the 2n passes on `stream`; *pass_count = 2n. first_slice/last_slice
+ * allow running a prefix (light_trace support): passes for k in [first, last). */
+int sbrc_half_angle(const sbrc_half_angle_params* p, int first_slice, int last_slice, int init, int finish,
+                    int* pass_count, void* stream);
 
 /* Number of rank-local image rows sbrc_render writes for (height, band_rows, rank, world). */
 int sbrc_local_rows(int height, int band_rows, int rank, int world);

@@ -26,6 +26,7 @@ the same float64 operation order so that results agree bit for bit:
 - ``phong_scalar``       raycaster.py:204-220
 - ``light_march``        raycaster.py:312-353 (_extinction_scalar, _shadow_oracle_scalar)
 - ``shadow_oracle``      raycaster.py:356-366 (shadow_oracle_many)
+- ``half_angle``         halfangle.py:35-142 (render_half_angle)
 
 Deliberate restatement choices (semantics-neutral):
 the build evaluates every texel of each slice instead of the polygon's
@@ -449,3 +450,86 @@ def render_image(vol, tf_lut: np.ndarray, settings, buffer=None, rows=None, cols
                           np.asarray(cam.position, np.float64), dirs.reshape(-1, 3))
     img = flat.reshape(hh, ww, 4).astype(np.float32)
     return (img, samples) if return_samples else img
+
+
+# ------------------------------------------------------------ half-angle baseline
+def _plane_uv_axes(direction):
+    w = _unit(direction)
+    hint = np.array([0.0, 1.0, 0.0])
+    if abs(float(np.dot(hint, w))) > 1.0 - 1e-9:
+        hint = np.array([0.0, 0.0, 1.0])
+    u = _unit(np.cross(hint, w))
+    return u, _unit(np.cross(w, u))
+
+
+def half_angle(vol, tf_lut, settings, n_slices, light_resolution=None):
+    """(image, passes): eye and light pass per slice (halfangle.py:48-142)."""
+    light, cam = settings.light, settings.camera
+    w, h = settings.viewport
+    lw, lh = light_resolution or settings.viewport
+    view = _unit(np.asarray(cam.target, np.float64) - np.asarray(cam.position, np.float64))
+    ld = np.asarray(light.direction, np.float64)
+    if float(np.dot(view, ld)) >= 0.0:
+        s, f2b = view + ld, True
+    else:
+        s, f2b = -view + ld, False
+    half = ld.copy() if float(np.linalg.norm(s)) < 1e-9 else _unit(s)
+    if float(np.linalg.norm(s)) < 1e-9:
+        f2b = False
+    corners = np.array([[(i >> a) & 1 for a in range(3)] for i in range(8)], dtype=np.float64)
+    proj = corners @ half
+    dlo, dhi = float(proj.min()), float(proj.max())
+    delta = (dhi - dlo) / n_slices
+    offsets = dlo + (np.arange(n_slices, dtype=np.float64) + 0.5) * delta
+    au, av = _plane_uv_axes(ld)
+    pu, pv = corners @ au, corners @ av
+    u0, u1, v0, v1 = float(pu.min()), float(pu.max()), float(pv.min()), float(pv.max())
+    uc = u0 + (np.arange(lw, dtype=np.float64) + 0.5) / lw * (u1 - u0)
+    vc = v0 + (np.arange(lh, dtype=np.float64) + 0.5) / lh * (v1 - v0)
+    ug, vg = np.meshgrid(uc, vc)
+    lbase = ug[..., None] * au + vg[..., None] * av
+    hl, hu, hv = float(np.dot(half, ld)), float(np.dot(half, au)), float(np.dot(half, av))
+    eye = np.asarray(cam.position, np.float64)
+    dirs = camera_rays(cam.position, cam.target, cam.up, cam.fov_deg, settings.viewport).reshape(-1, 3)
+    hd = dirs @ half
+    he = float(np.dot(half, eye))
+    acc = np.zeros((h * w, 4))
+    trans = np.ones((lh, lw))
+    lut = tf_lut
+    passes = 0
+    for k in range(n_slices):
+        off = float(offsets[k])
+        with np.errstate(divide="ignore", invalid="ignore"):
+            t = (off - he) / hd
+        pts = eye + t[:, None] * dirs
+        ok = (hd != 0) & (t > 0) & np.all((pts >= 0.0) & (pts <= 1.0), axis=1)
+        if ok.any():
+            p = pts[ok]
+            rgba = lut_blend(lut, trilinear(vol, p))
+            a = 1.0 - np.power(1.0 - rgba[:, 3], delta / (OPACITY_REF_STEP * np.abs(hd[ok])))
+            uv = np.stack([(p @ au - u0) / (u1 - u0), (p @ av - v0) / (v1 - v0)], axis=1)
+            tx, ty = uv[:, 0] * lw - 0.5, uv[:, 1] * lh - 0.5
+            xi, yi = np.floor(tx).astype(np.intp), np.floor(ty).astype(np.intp)
+            fx, fy = tx - xi, ty - yi
+            xa, xb = np.clip(xi, 0, lw - 1), np.clip(xi + 1, 0, lw - 1)
+            ya, yb = np.clip(yi, 0, lh - 1), np.clip(yi + 1, 0, lh - 1)
+            shade = ((trans[ya, xa] * (1 - fx) + trans[ya, xb] * fx) * (1 - fy)
+                     + (trans[yb, xa] * (1 - fx) + trans[yb, xb] * fx) * fy)
+            src = rgba[:, :3] * (a * shade)[:, None]
+            if f2b:
+                one_m = (1.0 - acc[ok, 3])[:, None]
+                acc[ok, :3] += one_m * src
+                acc[ok, 3] += one_m[:, 0] * a
+            else:
+                acc[ok, :3] = (1.0 - a)[:, None] * acc[ok, :3] + src
+                acc[ok, 3] = a + (1.0 - a) * acc[ok, 3]
+        passes += 1
+        tl = (off - ug * hu - vg * hv) / hl
+        lp = lbase + tl[..., None] * ld
+        cov = np.all((lp >= 0.0) & (lp <= 1.0), axis=-1)
+        if cov.any():
+            rgba = lut_blend(lut, trilinear(vol, lp[cov]))
+            a = 1.0 - np.power(1.0 - rgba[:, 3], delta / (OPACITY_REF_STEP * hl))
+            trans[cov] *= 1.0 - a
+        passes += 1
+    return acc.reshape(h, w, 4).astype(np.float32), passes

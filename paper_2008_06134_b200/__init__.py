@@ -41,3 +41,4 @@ from .raycaster import (  # noqa: F401
     shadow_oracle_many,
 )
 from .device import DeviceVolume, device_volume  # noqa: F401
+from .halfangle import render_half_angle  # noqa: F401

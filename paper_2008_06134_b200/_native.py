@@ -29,7 +29,7 @@ LOOKUP = {"linear": 0, "nearest": 1}
 #: every symbol include/sbrc.h declares
 EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume_check",
            "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_pack_octets", "sbrc_shadow_oracle", "sbrc_light_factor",
-           "sbrc_local_rows")
+           "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_local_rows")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -71,6 +71,17 @@ class SbrcRenderParams(C.Structure):
                 ("image", C.c_void_p), ("sample_count", C.c_void_p)]
 
 
+class SbrcHalfAngleParams(C.Structure):
+    _fields_ = [("volume", SbrcVolume), ("lut", C.c_void_p), ("plane_offsets", C.c_void_p),
+                ("width", C.c_int32), ("height", C.c_int32), ("light_width", C.c_int32),
+                ("light_height", C.c_int32), ("n_slices", C.c_int32), ("front_to_back", C.c_int32),
+                ("eye", D3), ("forward", D3), ("right", D3), ("up2", D3), ("tan_half", C.c_double),
+                ("aspect", C.c_double), ("half", D3), ("delta", C.c_double), ("light_dir", D3), ("axis_u", D3),
+                ("axis_v", D3), ("u_range", D2), ("v_range", D2), ("hl", C.c_double), ("h_dot_u", C.c_double),
+                ("h_dot_v", C.c_double), ("h_dot_e", C.c_double), ("eye_accum", C.c_void_p),
+                ("light_accum", C.c_void_p), ("image", C.c_void_p)]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -88,6 +99,9 @@ def _load() -> C.CDLL:
     lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
     lib.sbrc_light_factor.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
+    lib.sbrc_half_angle.argtypes = [C.POINTER(SbrcHalfAngleParams), C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(C.c_int), C.c_void_p]
+    lib.sbrc_normalize_f32.argtypes = [C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_void_p]
     lib.sbrc_pack_octets.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p]
     lib.sbrc_shadow_oracle.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_double, C.c_void_p, C.c_void_p]
@@ -95,7 +109,7 @@ def _load() -> C.CDLL:
                                     C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
     if lib.sbrc_abi_version() != ABI_VERSION:
         raise ImportError(f"sbrc ABI mismatch: library {lib.sbrc_abi_version()} != binding {ABI_VERSION}")
-    sizes = (SbrcVolume, SbrcLightFrame, SbrcBuildParams, SbrcRenderParams)
+    sizes = (SbrcVolume, SbrcLightFrame, SbrcBuildParams, SbrcRenderParams, SbrcHalfAngleParams)
     for i, st in enumerate(sizes):
         if lib.sbrc_struct_size(i) != C.sizeof(st):
             raise ImportError(f"sbrc struct {st.__name__} layout mismatch: "

@@ -1056,6 +1056,134 @@ __global__ void __launch_bounds__(256) light_factor_kernel(const sbrc_render_par
   out[i] = make_float4(scalar, f[0], f[1], f[2]);
 }
 
+// load_raw's float32 min-max normalisation (volume.py:147-151) in place:
+// numpy evaluates (flat - lo) / (hi - lo) in float32 (NEP 50: the Python
+// scalars become float32), i.e. fl32(fl32(x - lo) / fl32(hi - lo)).
+__global__ void __launch_bounds__(256) normalize_f32_kernel(float* data, long long n, float lo, float range) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    data[i] = __fdiv_rn(__fsub_rn(data[i], lo), range);
+}
+
+// ---------------------------------------------------------------- half-angle baseline
+// halfangle.py:48-142. Float64 throughout, reference op order for the slice
+// geometry; alpha correction a = 1 - (1 - alpha)^exponent via pow.
+__device__ __forceinline__ double lut_alpha_raw(const double* lut, double s, double* rgb) {
+  const LutPos q = lut_pos(s);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) rgb[c] = dadd(dmul(lut[4 * q.i0 + c], q.g), dmul(lut[4 * q.i1 + c], q.f));
+  return dadd(dmul(lut[4 * q.i0 + 3], q.g), dmul(lut[4 * q.i1 + 3], q.f));
+}
+
+__global__ void has_init_kernel(double* eye_accum, long long ne, double* light_accum, long long nl) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += (long long)gridDim.x * blockDim.x)
+    eye_accum[i] = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += (long long)gridDim.x * blockDim.x)
+    light_accum[i] = 1.0;
+}
+
+template <int VT, bool UNIT>
+__global__ void __launch_bounds__(256) has_eye_kernel(const sbrc_half_angle_params P, int k) {
+  __shared__ double lut[SBRC_LUT_SIZE * 4];
+  __shared__ double u8tab[256];
+  for (int i = threadIdx.x; i < SBRC_LUT_SIZE * 4; i += blockDim.x) lut[i] = P.lut[i];
+  if (std::is_same<typename Voxel<VT>::T, unsigned char>::value) fill_u8_table(u8tab);
+  __syncthreads();
+  const int px = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int py = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (px >= P.width || py >= P.height) return;
+  // Camera.rays (raycaster.py:53-68)
+  const double ndc_x = dmul(dmul(dsub(dmul(ddiv(dadd((double)px, 0.5), (double)P.width), 2.0), 1.0), P.tan_half),
+                            P.aspect);
+  const double ndc_y = dmul(dsub(1.0, dmul(ddiv(dadd((double)py, 0.5), (double)P.height), 2.0)), P.tan_half);
+  double d[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) d[c] = dadd(dadd(P.forward[c], dmul(ndc_x, P.right[c])), dmul(ndc_y, P.up2[c]));
+  const double nrm = __dsqrt_rn(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
+#pragma unroll
+  for (int c = 0; c < 3; ++c) d[c] = ddiv(d[c], nrm);
+  const double hdd = dadd(dadd(dmul(d[0], P.half[0]), dmul(d[1], P.half[1])), dmul(d[2], P.half[2]));
+  if (hdd == 0.0) return;
+  const double t = ddiv(dsub(P.plane_offsets[k], P.h_dot_e), hdd);  // :107
+  if (!(t > 0.0)) return;
+  const double q[3] = {dadd(P.eye[0], dmul(t, d[0])), dadd(P.eye[1], dmul(t, d[1])), dadd(P.eye[2], dmul(t, d[2]))};
+  if (!in_cube(q[0], q[1], q[2])) return;  // :109
+  const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), q[0], q[1], q[2]);
+  double rgb[3];
+  const double alpha_raw = lut_alpha_raw(lut, s, rgb);
+  const double expo = ddiv(P.delta, dmul(1.0 / 256.0, fabs(hdd)));  // :115
+  const double a = dsub(1.0, pow(dsub(1.0, alpha_raw), expo));
+  // light transmittance at the sample: _bilinear_scalar of light_accum at uv (:117-118)
+  const double u = ((q[0] * P.axis_u[0] + q[1] * P.axis_u[1] + q[2] * P.axis_u[2]) - P.u_range[0]) /
+                   (P.u_range[1] - P.u_range[0]);
+  const double v = ((q[0] * P.axis_v[0] + q[1] * P.axis_v[1] + q[2] * P.axis_v[2]) - P.v_range[0]) /
+                   (P.v_range[1] - P.v_range[0]);
+  const int W = P.light_width, H = P.light_height;
+  const double tx = u * W - 0.5, ty = v * H - 0.5;
+  const double fx0 = floor(tx), fy0 = floor(ty);
+  const double fx = tx - fx0, fy = ty - fy0;
+  const int x0 = (int)fx0, y0 = (int)fy0;
+  const int xa = min(max(x0, 0), W - 1), xb = min(max(x0 + 1, 0), W - 1);
+  const int ya = min(max(y0, 0), H - 1), yb = min(max(y0 + 1, 0), H - 1);
+  const double* L = P.light_accum;
+  const double c0 = L[(size_t)ya * W + xa] * (1 - fx) + L[(size_t)ya * W + xb] * fx;
+  const double c1 = L[(size_t)yb * W + xa] * (1 - fx) + L[(size_t)yb * W + xb] * fx;
+  const double shade = c0 * (1 - fy) + c1 * fy;
+  double* acc = P.eye_accum + 4 * ((size_t)py * P.width + px);
+  const double as = dmul(a, shade);
+  if (P.front_to_back) {  // :120-123
+    const double one_m = dsub(1.0, acc[3]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] = dadd(acc[c], dmul(one_m, dmul(rgb[c], as)));
+    acc[3] = dadd(acc[3], dmul(one_m, a));
+  } else {  // :124-126
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] = dadd(dmul(dsub(1.0, a), acc[c]), dmul(rgb[c], as));
+    acc[3] = dadd(a, dmul(dsub(1.0, a), acc[3]));
+  }
+}
+
+template <int VT, bool UNIT>
+__global__ void __launch_bounds__(256) has_light_kernel(const sbrc_half_angle_params P, int k) {
+  __shared__ double alut[SBRC_LUT_SIZE];
+  __shared__ double u8tab[256];
+  for (int i = threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x) alut[i] = P.lut[4 * i + 3];
+  if (std::is_same<typename Voxel<VT>::T, unsigned char>::value) fill_u8_table(u8tab);
+  __syncthreads();
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (x >= P.light_width || y >= P.light_height) return;
+  const double ug = dadd(P.u_range[0], dmul(ddiv(dadd((double)x, 0.5), (double)P.light_width),
+                                            dsub(P.u_range[1], P.u_range[0])));
+  const double vg = dadd(P.v_range[0], dmul(ddiv(dadd((double)y, 0.5), (double)P.light_height),
+                                            dsub(P.v_range[1], P.v_range[0])));
+  const double tl = ddiv(dsub(dsub(P.plane_offsets[k], dmul(ug, P.h_dot_u)), dmul(vg, P.h_dot_v)), P.hl);  // :130
+  double q[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    q[c] = dadd(dadd(dmul(ug, P.axis_u[c]), dmul(vg, P.axis_v[c])), dmul(tl, P.light_dir[c]));  // :131
+  if (!in_cube(q[0], q[1], q[2])) return;
+  const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), q[0], q[1], q[2]);
+  const LutPos lp = lut_pos(s);
+  const double alpha_raw = dadd(dmul(alut[lp.i0], lp.g), dmul(alut[lp.i1], lp.f));
+  const double a = dsub(1.0, pow(dsub(1.0, alpha_raw), ddiv(P.delta, dmul(1.0 / 256.0, P.hl))));  // :136
+  double* T = P.light_accum + (size_t)y * P.light_width + x;
+  *T = dmul(*T, dsub(1.0, a));
+}
+
+__global__ void has_finish_kernel(const double* eye_accum, float* image, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    image[i] = (float)eye_accum[i];
+}
+
+template <int VT, bool UNIT>
+void has_passes(const sbrc_half_angle_params& p, int k0, int k1, cudaStream_t s) {
+  const dim3 ge((p.width + 31) / 32, (p.height + 7) / 8), gl((p.light_width + 31) / 32, (p.light_height + 7) / 8);
+  for (int k = k0; k < k1; ++k) {
+    has_eye_kernel<VT, UNIT><<<ge, 256, 0, s>>>(p, k);
+    has_light_kernel<VT, UNIT><<<gl, 256, 0, s>>>(p, k);
+  }
+}
+
 // ---------------------------------------------------------------- dispatch
 bool volume_ok(const sbrc_volume& v) {
   if (v.data == nullptr) return false;
@@ -1166,6 +1294,7 @@ int64_t sbrc_struct_size(int which) {
     case 1: return (int64_t)sizeof(sbrc_light_frame);
     case 2: return (int64_t)sizeof(sbrc_build_params);
     case 3: return (int64_t)sizeof(sbrc_render_params);
+    case 4: return (int64_t)sizeof(sbrc_half_angle_params);
     default: return -1;
   }
 }
@@ -1207,6 +1336,13 @@ int sbrc_pack_quads(const float* plain, int64_t plain_layer_stride, int64_t plai
   dim3 grid((width + 31) / 32, (height + 7) / 8);
   pack_quads_kernel<<<grid, block, 0, s>>>(plain, plain_layer_stride, plain_row_stride, n, height, width, quads,
                                            quad_layer_stride, quad_row_stride);
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_normalize_f32(float* data, int64_t n, float lo, float range, void* stream) {
+  if (data == nullptr || n < 0 || !(range > 0.0f)) return SBRC_EINVAL;
+  if (n == 0) return SBRC_OK;
+  normalize_f32_kernel<<<148 * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(data, n, lo, range);
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 
@@ -1254,6 +1390,34 @@ int sbrc_light_factor(const sbrc_render_params* p, const double* pts, int64_t m,
     light_factor_kernel<SBRC_LOOKUP_NEAREST><<<blocks, 256, 0, s>>>(*p, pts, m, he, ex, ey, ez, reinterpret_cast<float4*>(out));
   else
     light_factor_kernel<SBRC_LOOKUP_LINEAR><<<blocks, 256, 0, s>>>(*p, pts, m, he, ex, ey, ez, reinterpret_cast<float4*>(out));
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_half_angle(const sbrc_half_angle_params* p, int first_slice, int last_slice, int init, int finish,
+                    int* pass_count, void* stream) {
+  if (p == nullptr || !volume_ok(p->volume) || p->lut == nullptr || p->plane_offsets == nullptr) return SBRC_EINVAL;
+  if (p->width < 1 || p->height < 1 || p->light_width < 1 || p->light_height < 1 || p->n_slices < 1)
+    return SBRC_EINVAL;
+  if (p->eye_accum == nullptr || p->light_accum == nullptr || p->image == nullptr || !(p->hl > 0.0))
+    return SBRC_EINVAL;
+  if (first_slice < 0 || last_slice > p->n_slices || first_slice > last_slice) return SBRC_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const long long ne = 4ll * p->width * p->height, nl = (long long)p->light_width * p->light_height;
+  if (init) has_init_kernel<<<148 * 4, 256, 0, s>>>(p->eye_accum, ne, p->light_accum, nl);
+  const bool unit = unit_box(p->volume);
+  switch (p->volume.voxel_type) {
+#define SBRC_HAS(VT) (unit ? has_passes<VT, true>(*p, first_slice, last_slice, s) \
+                           : has_passes<VT, false>(*p, first_slice, last_slice, s))
+    case SBRC_VOXEL_F32: SBRC_HAS(SBRC_VOXEL_F32); break;
+    case SBRC_VOXEL_U8: SBRC_HAS(SBRC_VOXEL_U8); break;
+    case SBRC_VOXEL_U16: SBRC_HAS(SBRC_VOXEL_U16); break;
+    case SBRC_VOXEL_F32_OCT: SBRC_HAS(SBRC_VOXEL_F32_OCT); break;
+    case SBRC_VOXEL_U8_OCT: SBRC_HAS(SBRC_VOXEL_U8_OCT); break;
+    default: SBRC_HAS(SBRC_VOXEL_U16_OCT); break;
+#undef SBRC_HAS
+  }
+  if (finish) has_finish_kernel<<<148 * 4, 256, 0, s>>>(p->eye_accum, p->image, ne);
+  if (pass_count) *pass_count = 2 * (last_slice - first_slice);
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 

@@ -387,3 +387,25 @@ def test_phong_extinction_and_shadow_oracle(sb):
         got = sb.shadow_oracle_many(v, tf, g["probe"], light, m["oracle_step"])
         want = g["oracle_aniso" if aniso else "oracle"]
         assert np.abs(got - want).max() <= 1e-12
+
+
+@pytest.mark.parametrize("tag", ["f2b", "b2f"])
+def test_half_angle_baseline(sb, tag):
+    """GPU half-angle slicing vs the reference (halfangle.py:48-142): image,
+    pass count 2n, and the light transmittance after every slice."""
+    g = load_golden("half_angle")
+    m = g["meta"]
+    c = m["cases"][tag]
+    v = sb.VolumeDataset.from_array(g["volume"])
+    s = sb.RenderSettings(camera=sb.Camera(position=c["pos"], target=(0.5, 0.5, 0.5), fov_deg=45.0),
+                          light=sb.Light(direction=c["light"]), viewport=tuple(m["viewport"]), step=1 / 64)
+    img, passes = sb.render_half_angle(v, sb.preset(m["tf"]), s, m["n"], light_resolution=tuple(m["light_res"]))
+    assert passes == 2 * m["n"]
+    st = parity_stats(img, g[f"image_{tag}"])
+    _report(f"half-angle {tag}", st)
+    assert st["max_abs"] <= 1e-6
+    trace = []
+    img2, _ = sb.render_half_angle(v, sb.preset(m["tf"]), s, m["n"], light_resolution=tuple(m["light_res"]),
+                                   light_trace=trace)
+    assert np.array_equal(img, img2) and len(trace) == m["n"]
+    assert np.abs(np.stack(trace) - g[f"trace_{tag}"]).max() <= 1e-12

@@ -137,3 +137,24 @@ def test_extra_modes_bit_exact():
         assert np.array_equal(O.shadow_oracle(v, tf.lut, g["probe"], light.direction, g["meta"]["oracle_step"]), want)
     v, *_ = _extra_scene(g, True)
     assert np.array_equal(O.gradient(v, g["probe"]), g["grad"])
+
+
+def _has_scene(g, tag):
+    from paper_2008_06134_b200 import scene
+    m = g["meta"]
+    c = m["cases"][tag]
+    v = scene.VolumeDataset.from_array(g["volume"])
+    cam = scene.Camera(position=c["pos"], target=(0.5, 0.5, 0.5), fov_deg=45.0)
+    s = scene.RenderSettings(camera=cam, light=scene.Light(direction=c["light"]), viewport=tuple(m["viewport"]),
+                             step=1 / 64)
+    return v, scene.preset(m["tf"]), s, m, c
+
+
+@pytest.mark.parametrize("tag", ["f2b", "b2f"])
+def test_half_angle_oracle(tag):
+    """render_half_angle in both slice orders vs the reference (1e-12: BLAS dots)."""
+    g = load_golden("half_angle")
+    v, tf, s, m, c = _has_scene(g, tag)
+    img, passes = O.half_angle(v, tf.lut, s, m["n"], tuple(m["light_res"]))
+    assert passes == c["passes"] == 2 * m["n"]
+    np.testing.assert_allclose(img, g[f"image_{tag}"], rtol=0, atol=1e-6)
