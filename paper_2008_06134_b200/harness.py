@@ -30,7 +30,7 @@ from .lightbuffer import AttenuationBuffer, build_attenuation_buffer
 from .raycaster import render_device
 from .scene import BUFFER_MODES, LightCamera, RenderSettings, make_slice_stack
 
-#: bench/CLI method names -> shading modes (config.py:18-25); "has" is not on the GPU path
+#: bench/CLI method names -> shading modes (config.py:18-25); "has" = half-angle slicing (halfangle.py)
 METHOD_MODES = {"none": "none", "phong": "phong", "sbrc": "sbrc_shadow", "shell": "shell", "cone": "cone",
                 "extinction": "extinction"}
 
@@ -168,10 +168,22 @@ def image_sha256(img) -> str:
     return hashlib.sha256(np.ascontiguousarray(arr, dtype=np.float32).tobytes()).hexdigest()
 
 
+METHODS = tuple(METHOD_MODES) + ("has",)
+
+
 def render_scene(v, tf, settings, method: str, n_slices: int, resolution, compensation_n: float = 0.0):
     """bench.render_scene (bench.py:87-109) on the device: (image, build_ms, render_ms, pass_count)."""
-    if method not in METHOD_MODES:
-        raise ValueError(f"method {method!r} is not on the GPU path (choose from {sorted(METHOD_MODES)})")
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r} (choose from {METHODS})")
+    if method == "has":  # half-angle slicing: all of its cost is render (bench.py:90-95)
+        from .halfangle import render_half_angle
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        img, passes = render_half_angle(v, tf, settings, n_slices, light_resolution=resolution)
+        e1.record(stream)
+        e1.synchronize()
+        return img, 0.0, e0.elapsed_time(e1), passes
     mode = METHOD_MODES[method]
     s = RenderSettings(camera=settings.camera, light=settings.light, viewport=settings.viewport,
                        step=settings.step, shading_mode=mode,

@@ -124,3 +124,24 @@ def test_cached_build_skips_rebuild():
     assert (hit1, hit2) == (False, True) and b1 is b2
     assert np.array_equal(b1.intensity, g["intensity"])
     assert cache.bytes == 24 * 36 * 40 * 16
+
+
+@pytest.mark.gpu
+def test_acceptance_c4_trend_on_gpu():
+    """Acceptance C4 (reference tests/test_acceptance.py:148-165) with
+    device timing: SBRC render(256)/render(64) <= 1.5 and the half-angle total
+    grows >= 2.5x (pass count 2n)."""
+    from paper_2008_06134_b200.harness import run_sweep
+    from paper_2008_06134_b200.datasets import make_sphere_blobs
+    from paper_2008_06134_b200 import scene
+    v = make_sphere_blobs((128, 128, 128), seed=7)
+    tf = scene.preset("hot")
+    s = scene.RenderSettings(camera=scene.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5)),
+                             light=scene.Light(direction=(0.3, -0.5, 0.8)), viewport=(256, 256), step=1 / 256)
+    recs = {(r.method, r.n_slices): r for r in run_sweep(v, tf, s, ["sbrc", "has"], [64, 256], [256], repeats=3)}
+    sbrc_ratio = recs[("sbrc", 256)].render_ms / recs[("sbrc", 64)].render_ms
+    has_ratio = recs[("has", 256)].total_ms / recs[("has", 64)].total_ms
+    print(f"[c4] sbrc render ratio {sbrc_ratio:.2f}, has total ratio {has_ratio:.2f}, "
+          f"passes {recs[('has', 64)].pass_count}->{recs[('has', 256)].pass_count}")
+    assert sbrc_ratio <= 1.5 and has_ratio >= 2.5
+    assert recs[("has", 256)].pass_count == 512
