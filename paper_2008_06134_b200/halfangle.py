@@ -37,6 +37,13 @@ def render_half_angle(v, tf, settings, n_slices: int, light_resolution=None, lig
                       device=None):
     """(image (H, W, 4) float32 numpy, pass_count = 2n) — drop-in for halfangle.py:48-142.
     ``light_trace`` (a list) receives the light transmittance after every slice."""
+    img, passes = render_half_angle_device(v, tf, settings, n_slices, light_resolution, light_trace, device)
+    return to_host(img), passes
+
+
+def render_half_angle_device(v, tf, settings, n_slices: int, light_resolution=None, light_trace: list | None = None,
+                             device=None):
+    """As render_half_angle, returning the (H, W, 4) CUDA image (no host copy)."""
     if n_slices < 1:
         raise ValueError("n_slices must be >= 1")
     dev = _require_cuda(device)
@@ -84,4 +91,4 @@ def render_half_angle(v, tf, settings, n_slices: int, light_resolution=None, lig
                                           C.byref(count), stream), "sbrc_half_angle")
             total += count.value
             light_trace.append(to_host(light_acc).reshape(lh, lw).copy())
-    return to_host(image), total
+    return image, total

@@ -176,11 +176,11 @@ def render_scene(v, tf, settings, method: str, n_slices: int, resolution, compen
     if method not in METHODS:
         raise ValueError(f"unknown method {method!r} (choose from {METHODS})")
     if method == "has":  # half-angle slicing: all of its cost is render (bench.py:90-95)
-        from .halfangle import render_half_angle
+        from .halfangle import render_half_angle_device
         stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        img, passes = render_half_angle(v, tf, settings, n_slices, light_resolution=resolution)
+        img, passes = render_half_angle_device(v, tf, settings, n_slices, light_resolution=resolution)
         e1.record(stream)
         e1.synchronize()
         return img, 0.0, e0.elapsed_time(e1), passes

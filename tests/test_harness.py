@@ -138,7 +138,9 @@ def test_acceptance_c4_trend_on_gpu():
     tf = scene.preset("hot")
     s = scene.RenderSettings(camera=scene.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5)),
                              light=scene.Light(direction=(0.3, -0.5, 0.8)), viewport=(256, 256), step=1 / 256)
-    recs = {(r.method, r.n_slices): r for r in run_sweep(v, tf, s, ["sbrc", "has"], [64, 256], [256], repeats=3)}
+    recs = {(r.method, r.n_slices): r for r in run_sweep(v, tf, s, ["sbrc", "has"], [64, 256], [256], repeats=5)}
+    for r in recs.values():
+        print(f"[c4] {r.method} n={r.n_slices} build {r.build_ms:.3f} render {r.render_ms:.3f} ms")
     sbrc_ratio = recs[("sbrc", 256)].render_ms / recs[("sbrc", 64)].render_ms
     has_ratio = recs[("has", 256)].total_ms / recs[("has", 64)].total_ms
     print(f"[c4] sbrc render ratio {sbrc_ratio:.2f}, has total ratio {has_ratio:.2f}, "
