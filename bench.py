@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--mode", default=None, help="override shading mode")
     ap.add_argument("--build", choices=("replicated", "sharded"), default="replicated")
+    ap.add_argument("--assemble", choices=("p2p", "nccl"), default="p2p",
+                    help="N>1 image assembly: fused peer-memory stores from the march kernel (self-checked, "
+                         "falls back to NCCL) or NCCL all-gather")
     ap.add_argument("--voxel", choices=("linear", "octet"), default="linear",
                     help="device layout of the volume: linear (x-fastest) or octets (8 corners per cell)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -349,7 +352,7 @@ def run_ours(a, cfg, mode):
     torch.cuda.synchronize()
     vol_gen_s = time.perf_counter() - t0
     fr = FrameRenderer(dvol, tf, cam, spec, settings, build=a.build if world > 1 else "replicated",
-                       band_rows=8, device=dev)
+                       band_rows=8, device=dev, assemble=a.assemble)
     stream = torch.cuda.current_stream()
 
     # samples per frame (deterministic): one counted frame
@@ -438,6 +441,7 @@ def run_ours(a, cfg, mode):
                        "image": [cfg["image"], cfg["image"]], "n_slices": cfg["n"],
                        "slice_res": [cfg["res"], cfg["res"]], "step": cfg["step"], "shading_mode": mode,
                        "build": a.build if world > 1 else "single", "parallelism": f"image-tiles x{world}",
+                       "assemble": fr.assemble_mode if world > 1 else "none",
                        "l2": "inputs larger than L2 (volume %d MiB, buffer %d MiB)" % (V >> 20, A >> 20)},
             "gsamples_per_s": samples / (k2_ms * 1e-3) / 1e9,
             "samples_per_frame": samples,
@@ -453,6 +457,7 @@ def run_ours(a, cfg, mode):
             "volume_gen_s": vol_gen_s,
         }
         print(json.dumps(line), flush=True)
+    fr.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

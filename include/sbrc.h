@@ -41,6 +41,7 @@ extern "C" {
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
+#define SBRC_MAX_PEERS 8    /* GPUs of one node (image assembly over peer memory) */
 
 typedef enum sbrc_status {
   SBRC_OK = 0,
@@ -152,7 +153,14 @@ typedef struct sbrc_render_params {
   double scene_light_dir[3];       /* Light.direction (normalised)        */
   double phong[4];                 /* PhongParams: ambient, diffuse, specular, shininess */
   double voxel_size[3];            /* VolumeDataset.voxel_size (gradient steps, volume.py:210) */
-  float* image;                    /* device, rank-local (rows, W, 4) premultiplied rgba */
+  float* image;                    /* device, rank-local (rows, W, 4) premultiplied rgba; may be
+                                      NULL when n_peers > 0 */
+  /* Fused image assembly over peer memory: when n_peers > 0 every finished
+   * pixel (px, py) is also stored to peer_images[i][py*W + px] (float4) for
+   * i < n_peers — the full raster images of all ranks, mapped into this
+   * process (CUDA IPC over NVLink). The caller then needs only a barrier. */
+  float* peer_images[SBRC_MAX_PEERS];
+  int32_t n_peers, _pad3;
   unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
 } sbrc_render_params;
 
@@ -237,6 +245,16 @@ typedef struct sbrc_half_angle_params {
  * allow running a prefix (light_trace support): passes for k in [first, last). */
 int sbrc_half_angle(const sbrc_half_angle_params* p, int first_slice, int last_slice, int init, int finish,
                     int* pass_count, void* stream);
+
+/* Peer-memory plumbing for the fused image assembly (one process per GPU):
+ * an IPC-capable allocation, its 64-byte handle, and mapping a peer's handle
+ * into this process with lazy peer access (NVLink). These are the only
+ * entry points that allocate or map memory. */
+int sbrc_ipc_alloc(int64_t bytes, void** ptr);
+int sbrc_ipc_free(void* ptr);
+int sbrc_ipc_handle(void* ptr, unsigned char handle[64]);
+int sbrc_ipc_open(const unsigned char handle[64], void** ptr);
+int sbrc_ipc_close(void* ptr);
 
 /* Number of rank-local image rows sbrc_render writes for (height, band_rows, rank, world). */
 int sbrc_local_rows(int height, int band_rows, int rank, int world);

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC
 ABI_VERSION = 2
 MAX_SHELLS = 8
 MAX_ANGLES = 16
+MAX_PEERS = 8
 
 OK, EINVAL, ECONFIG, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4
 VOXEL_F32, VOXEL_U8, VOXEL_U16 = 0, 1, 2
@@ -29,7 +30,8 @@ LOOKUP = {"linear": 0, "nearest": 1}
 #: every symbol include/sbrc.h declares
 EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume_check",
            "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_pack_octets", "sbrc_shadow_oracle", "sbrc_light_factor",
-           "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_local_rows")
+           "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_ipc_alloc", "sbrc_ipc_free", "sbrc_ipc_handle",
+           "sbrc_ipc_open", "sbrc_ipc_close", "sbrc_local_rows")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -68,7 +70,8 @@ class SbrcRenderParams(C.Structure):
                 ("cone_sin", C.c_double * MAX_ANGLES),
                 ("band_rows", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("local_rows", C.c_int32),
                 ("scene_light_dir", D3), ("phong", C.c_double * 4), ("voxel_size", D3),
-                ("image", C.c_void_p), ("sample_count", C.c_void_p)]
+                ("image", C.c_void_p), ("peer_images", C.c_void_p * MAX_PEERS), ("n_peers", C.c_int32),
+                ("_pad3", C.c_int32), ("sample_count", C.c_void_p)]
 
 
 class SbrcHalfAngleParams(C.Structure):
@@ -99,6 +102,11 @@ def _load() -> C.CDLL:
     lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
     lib.sbrc_light_factor.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
+    lib.sbrc_ipc_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
+    lib.sbrc_ipc_free.argtypes = [C.c_void_p]
+    lib.sbrc_ipc_handle.argtypes = [C.c_void_p, C.c_char * 64]
+    lib.sbrc_ipc_open.argtypes = [C.c_char * 64, C.POINTER(C.c_void_p)]
+    lib.sbrc_ipc_close.argtypes = [C.c_void_p]
     lib.sbrc_half_angle.argtypes = [C.POINTER(SbrcHalfAngleParams), C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(C.c_int), C.c_void_p]
     lib.sbrc_normalize_f32.argtypes = [C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_void_p]

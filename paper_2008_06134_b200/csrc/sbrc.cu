@@ -31,6 +31,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include <type_traits>
 
@@ -917,8 +918,15 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
       result = make_float4((float)cr, (float)cg, (float)cb, (float)alpha);
     }
   }
-  if (in_image)  // background (and padding rows of a partial last band) is transparent black
-    reinterpret_cast<float4*>(P.image)[(size_t)lr * P.width + px] = result;
+  if (in_image) {  // background (and padding rows of a partial last band) is transparent black
+    if (P.image != nullptr) reinterpret_cast<float4*>(P.image)[(size_t)lr * P.width + px] = result;
+    // fused assembly: the pixel goes straight into every rank's raster image
+    // (peer memory over NVLink); a barrier after the kernel completes the frame
+    if (valid)
+      for (int i = 0; i < P.n_peers; ++i)
+        reinterpret_cast<float4*>(P.peer_images[i])[(size_t)py * P.width + px] = result;
+  }
+  if (P.n_peers > 0) __threadfence_system();
   if (P.sample_count != nullptr) {
     const unsigned int tot = __reduce_add_sync(0xffffffffu, samples);
     if (lane == 0 && tot) atomicAdd(P.sample_count, (unsigned long long)tot);
@@ -1301,6 +1309,31 @@ int64_t sbrc_struct_size(int which) {
 
 int sbrc_volume_check(const sbrc_volume* v) { return (v && volume_ok(*v)) ? SBRC_OK : SBRC_EINVAL; }
 
+int sbrc_ipc_alloc(int64_t bytes, void** ptr) {
+  if (ptr == nullptr || bytes <= 0) return SBRC_EINVAL;
+  return cudaMalloc(ptr, (size_t)bytes) == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_ipc_free(void* ptr) { return cudaFree(ptr) == cudaSuccess ? SBRC_OK : SBRC_ECUDA; }
+
+int sbrc_ipc_handle(void* ptr, unsigned char handle[64]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (ptr == nullptr || handle == nullptr) return SBRC_EINVAL;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, ptr) != cudaSuccess) return SBRC_ECUDA;
+  memcpy(handle, &h, sizeof(h));
+  return SBRC_OK;
+}
+
+int sbrc_ipc_open(const unsigned char handle[64], void** ptr) {
+  if (ptr == nullptr || handle == nullptr) return SBRC_EINVAL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_ipc_close(void* ptr) { return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? SBRC_OK : SBRC_ECUDA; }
+
 int sbrc_local_rows(int height, int band_rows, int rank, int world) {
   if (height < 1 || band_rows < 1 || world < 1 || rank < 0 || rank >= world) return 0;
   const int bands = (height + band_rows - 1) / band_rows;
@@ -1451,7 +1484,10 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
   if (p == nullptr || !volume_ok(p->volume)) return SBRC_EINVAL;
   if (p->width < 1 || p->height < 1 || !(p->step > 0.0)) return SBRC_EINVAL;           // raycaster.py:143-146
   if (!(p->et_alpha > 0.0 && p->et_alpha <= 1.0)) return SBRC_EINVAL;                  // :147-148
-  if (p->lut_rgba == nullptr || p->image == nullptr) return SBRC_EINVAL;
+  if (p->lut_rgba == nullptr || p->n_peers < 0 || p->n_peers > SBRC_MAX_PEERS) return SBRC_EINVAL;
+  if (p->image == nullptr && p->n_peers == 0) return SBRC_EINVAL;
+  for (int i = 0; i < p->n_peers; ++i)
+    if (p->peer_images[i] == nullptr) return SBRC_EINVAL;
   if (p->shading < SBRC_SHADE_NONE || p->shading > SBRC_SHADE_EXTINCTION) return SBRC_EUNSUPPORTED;
   if (p->lookup != SBRC_LOOKUP_LINEAR && p->lookup != SBRC_LOOKUP_NEAREST) return SBRC_EINVAL;
   if (p->band_rows < 1 || p->band_rows % 8 != 0 || p->world < 1 || p->rank < 0 || p->rank >= p->world)

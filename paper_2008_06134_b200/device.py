@@ -195,7 +195,8 @@ def pack_quads(plain: torch.Tensor, quads: torch.Tensor | None = None) -> torch.
 def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_cam, buffer_spec,
                   quads_dev: torch.Tensor | None, light_color, voxel_size_max: float,
                   image: torch.Tensor, counter: torch.Tensor | None,
-                  band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None) -> N.SbrcRenderParams:
+                  band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
+                  peer_images=()) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469)."""
     mode = settings.shading_mode
     if mode not in N.SHADE:
@@ -248,6 +249,11 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
         for i, th in enumerate(k.angles):
             p.cone_cos[i], p.cone_sin[i] = math.cos(th), math.sin(th)
     p.band_rows, p.rank, p.world = int(band_rows), int(rank), int(world)
-    p.image = image.data_ptr()
+    p.image = image.data_ptr() if image is not None else None
+    if len(peer_images) > N.MAX_PEERS:
+        raise ValueError(f"at most {N.MAX_PEERS} peer images")
+    for i, ptr in enumerate(peer_images):
+        p.peer_images[i] = int(ptr)
+    p.n_peers = len(peer_images)
     p.sample_count = counter.data_ptr() if counter is not None else None
     return p

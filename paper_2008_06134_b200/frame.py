@@ -24,6 +24,8 @@ Partitioning:
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -56,20 +58,56 @@ def shard_rows(height: int, world: int, rank: int) -> tuple[int, int, int]:
 
 def all_gather_into(out: torch.Tensor, chunk: torch.Tensor, group=None) -> None:
     """``out`` = concatenation of every rank's ``chunk`` along dim 0."""
-    if out.device.type == "cuda" or dist.get_backend(group) == "nccl":
+    if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, chunk, group=group)
-    else:  # gloo (CPU tests)
-        parts = list(out.view(-1, *chunk.shape).unbind(0))
-        dist.all_gather(parts, chunk, group=group)
+        return
+    # gloo (tests): gather host copies
+    host = chunk.cpu()
+    parts = [torch.empty_like(host) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, host, group=group)
+    out.copy_(torch.cat(parts).view_as(out))
+
+
+class _DeviceBuffer:
+    """An IPC-capable cudaMalloc allocation exposed to torch via __cuda_array_interface__."""
+
+    def __init__(self, nbytes: int):
+        ptr = C.c_void_p()
+        N.check(N.lib.sbrc_ipc_alloc(nbytes, C.byref(ptr)), "sbrc_ipc_alloc")
+        self.ptr, self.nbytes = ptr.value, nbytes
+        self.__cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<f4", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+
+    def handle(self) -> bytes:
+        buf = (C.c_char * 64)()
+        N.check(N.lib.sbrc_ipc_handle(self.ptr, buf), "sbrc_ipc_handle")
+        return bytes(buf)
+
+    def free(self) -> None:
+        if self.ptr:
+            N.lib.sbrc_ipc_free(self.ptr)
+            self.ptr = None
+
+
+def open_peer(handle: bytes) -> int:
+    ptr = C.c_void_p()
+    N.check(N.lib.sbrc_ipc_open((C.c_char * 64).from_buffer_copy(handle), C.byref(ptr)), "sbrc_ipc_open")
+    return ptr.value
 
 
 class FrameRenderer:
     """Build + march + assemble one frame of a fixed scene, all on device.
 
-    ``build`` is "replicated" or "sharded" (row-sharded K1 + all-gather)."""
+    ``build`` is "replicated" or "sharded" (row-sharded K1 + all-gather).
+    ``assemble`` is "nccl" (compact chunks + all_gather_into_tensor + row
+    permutation) or "p2p": the march kernel stores every finished pixel
+    straight into each rank's raster image through CUDA-IPC peer mappings
+    (NVLink), so the frame ends with a barrier instead of an all-gather. The
+    p2p mode verifies itself against the NCCL path on the first frame and
+    falls back to it (``assemble_mode``) if the images differ."""
 
     def __init__(self, volume, tf, light_cam, spec, settings, *, group=None, build: str = "replicated",
-                 band_rows: int = 8, compensation_n: float = 0.0, device=None):
+                 band_rows: int = 8, compensation_n: float = 0.0, device=None, assemble: str = "nccl"):
         check_frame(light_cam, spec)
         if build not in ("replicated", "sharded"):
             raise ValueError(f"build must be 'replicated' or 'sharded', got {build!r}")
@@ -96,6 +134,50 @@ class FrameRenderer:
         else:
             self.image = self.chunk[:h]
         self.set_light(light_cam, spec)
+        if assemble not in ("nccl", "p2p"):
+            raise ValueError(f"assemble must be 'nccl' or 'p2p', got {assemble!r}")
+        self.assemble_mode = "nccl"
+        self._peers: list[int] = []
+        if assemble == "p2p" and self.world > 1:
+            self._setup_p2p()
+
+    # -------------------------------------------------------------- p2p
+    def _setup_p2p(self) -> None:
+        h, w = self.height, self.width
+        self._raster = _DeviceBuffer(h * w * 16)
+        raster = torch.as_tensor(self._raster, device=self.dev).view(h, w, 4)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self._raster.handle(), group=self.group)
+        peers, opened = [], []
+        try:
+            for r, hd in enumerate(handles):
+                if r == self.rank:
+                    peers.append(self._raster.ptr)
+                else:
+                    ptr = open_peer(hd)
+                    opened.append(ptr)
+                    peers.append(ptr)
+            ok = True
+        except RuntimeError:
+            ok = False
+        self._opened = opened
+        self._barrier = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        # self-check: one frame both ways must agree bit for bit on every rank
+        if ok:
+            ref = self.frame().clone()
+            self._peers = peers
+            self._raster_t = raster
+            self.assemble_mode = "p2p"
+            self._render_params = None
+            got = self.frame()
+            ok = bool(torch.equal(ref, got))
+        flag = torch.tensor([0 if ok else 1], dtype=torch.int32,
+                            device=self.dev if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+        if int(flag.item()) != 0:
+            self._peers = []
+            self.assemble_mode = "nccl"
+            self._render_params = None
 
     # -------------------------------------------------------------- light
     def prepare_light(self, light_cam, spec):
@@ -149,20 +231,41 @@ class FrameRenderer:
 
     def march(self, count_samples: bool = True) -> None:
         if self._render_params is None:
-            buf_modes = self.settings.shading_mode != "none"
+            buf_modes = self.settings.shading_mode in ("sbrc_shadow", "shell", "cone")
+            p2p = self.assemble_mode == "p2p"
             self._render_params = render_params(
                 self.dvol, self.lut, self.settings, self.cam if buf_modes else None,
                 self.spec if buf_modes else None, self.quads if buf_modes else None,
-                self.cam.light_color, float(self.dvol.voxel_size.max()), self.chunk, self.counter,
-                band_rows=self.band_rows, rank=self.rank, world=self.world)
+                self.cam.light_color, float(self.dvol.voxel_size.max()), None if p2p else self.chunk, self.counter,
+                band_rows=self.band_rows, rank=self.rank, world=self.world, voxel_size=self.dvol.voxel_size,
+                peer_images=self._peers if p2p else ())
         self._render_params.sample_count = self.counter.data_ptr() if count_samples else None
         N.check(N.lib.sbrc_render(self._render_params, current_stream_handle()), "sbrc_render")
 
     def assemble(self) -> torch.Tensor:
         if self.world > 1:
+            if self.assemble_mode == "p2p":
+                # every rank's march has stored its pixels into every raster image;
+                # the barrier (stream-ordered after the march) completes the frame
+                if dist.get_backend(self.group) == "nccl":
+                    dist.all_reduce(self._barrier, group=self.group)
+                else:  # gloo (tests): host barrier after this rank's march completed
+                    torch.cuda.current_stream(self.dev).synchronize()
+                    dist.barrier(group=self.group)
+                return self._raster_t
             all_gather_into(self.gathered, self.chunk, self.group)
             torch.index_select(self.gathered, 0, self.perm, out=self.image)
         return self.image
+
+    def close(self) -> None:
+        """Unmap peer images and free the IPC raster (p2p mode)."""
+        for ptr in getattr(self, "_opened", []):
+            N.lib.sbrc_ipc_close(ptr)
+        self._opened = []
+        if getattr(self, "_raster", None) is not None:
+            torch.cuda.synchronize(self.dev)
+            self._raster.free()
+            self._raster = None
 
     def frame(self) -> torch.Tensor:
         self.build()

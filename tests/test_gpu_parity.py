@@ -409,3 +409,22 @@ def test_half_angle_baseline(sb, tag):
                                    light_trace=trace)
     assert np.array_equal(img, img2) and len(trace) == m["n"]
     assert np.abs(np.stack(trace) - g[f"trace_{tag}"]).max() <= 1e-12
+
+
+def test_fused_peer_assembly_emulated(sb):
+    """The march's peer-memory stores (fused image assembly) put every rank's
+    pixels at their raster positions: ranks emulated one after another on one
+    GPU, all writing into one raster image (n_peers = 1), reassemble the
+    single-rank image bit for bit."""
+    import torch
+    g = load_golden("blob32")
+    v, tf, cam, spec, settings_for = scene_from_golden(g)
+    buf = sb.build_attenuation_buffer(v, tf, cam, spec)
+    s = settings_for("cone")
+    want = sb.render(v, tf, s, buf)
+    w, h = s.viewport
+    for world, br in ((2, 8), (3, 16), (4, 8)):
+        raster = torch.full((h, w, 4), -1.0, dtype=torch.float32, device="cuda")
+        for r in range(world):
+            sb.render_device(v, tf, s, buf, rank=r, world=world, band_rows=br, peer_images=[raster])
+        assert np.array_equal(raster.cpu().numpy(), want), world
