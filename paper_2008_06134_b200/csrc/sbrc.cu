@@ -36,6 +36,9 @@
 #include <type_traits>
 
 // Compile-time variants (A/B'd in profiles/r01_notes.md).
+#ifndef SBRC_CONE_RING_SERIAL
+#define SBRC_CONE_RING_SERIAL 0  // 1: one cone ring's loads in flight at a time (fewer registers)
+#endif
 #ifndef SBRC_BUILD_UNROLL
 #define SBRC_BUILD_UNROLL 2  // slices whose gathers are in flight together in K1
 #endif
@@ -847,7 +850,11 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
                               li - (float)CONE_A >= 0.f && li - 1.0f < fast_l_hi;
             if (fast) {
               // every tap inside the buffer: one layer pair per ring, blended once
+#if SBRC_CONE_RING_SERIAL
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
               for (int i = 1; i <= CONE_A; ++i) {
                 const float r = spacing_r * (float)i;
                 const float lt = li - (float)i;

@@ -428,3 +428,46 @@ def test_fused_peer_assembly_emulated(sb):
         for r in range(world):
             sb.render_device(v, tf, s, buf, rank=r, world=world, band_rows=br, peer_images=[raster])
         assert np.array_equal(raster.cpu().numpy(), want), world
+
+
+@pytest.mark.parametrize("case", ["eye_inside", "all_miss", "one_pixel", "no_termination", "tiny_threshold",
+                                  "grazing_light", "compensated_shell"])
+def test_geometry_edge_cases(sb, case):
+    """Edge cases of the reference geometry against the oracle (bit-exact
+    where no lookup is involved, 1e-4 otherwise)."""
+    from oracle import slicecast_oracle as O
+    from paper_2008_06134_b200.datasets import make_sphere_blobs
+    v = make_sphere_blobs((24, 24, 24), seed=9)
+    tf = sb.preset("hot")
+    ld, pos, target, fov, vp, et, mode, comp = (0.3, -0.5, 0.8), (0.5, 0.5, -1.6), (0.5, 0.5, 0.5), 45.0, (20, 16), \
+        0.99, "cone", 0.0
+    if case == "eye_inside":
+        pos, target, fov = (0.45, 0.55, 0.4), (0.9, 0.2, 0.8), 70.0
+    elif case == "all_miss":
+        pos, target = (0.5, 0.5, -1.6), (0.5, 0.5, -3.0)
+    elif case == "one_pixel":
+        vp = (1, 1)
+    elif case == "no_termination":
+        et = 1.0
+    elif case == "tiny_threshold":
+        et = 0.05
+    elif case == "grazing_light":
+        ld = (1.0, 1e-7, 0.0)
+    elif case == "compensated_shell":
+        mode, comp = "shell", 1.5
+    cam = sb.LightCamera.fit(ld, (1, 1, 1), (20, 18))
+    spec = sb.make_slice_stack(ld, 14)
+    buf = sb.build_attenuation_buffer(v, tf, cam, spec, compensation_n=comp)
+    want_stack = O.build_intensity(v, tf.lut, cam, spec, comp)
+    assert np.abs(buf.intensity - want_stack).max() <= (1e-6 if comp else 0.0)
+    for m in ("none", mode):
+        s = sb.RenderSettings(camera=sb.Camera(position=pos, target=target, fov_deg=fov), light=sb.Light(direction=ld),
+                              viewport=vp, step=1 / 40, shading_mode=m, early_termination_alpha=et)
+        got = sb.render(v, tf, s, buf if m != "none" else None)
+        want = O.render_image(v, tf.lut, s, buf if m != "none" else None)
+        if m == "none":
+            assert np.array_equal(got, want), (case, m)
+        else:
+            assert parity_stats(got, want)["max_abs"] <= TIGHT, (case, m)
+        if case == "all_miss":
+            assert np.all(got == 0.0)
