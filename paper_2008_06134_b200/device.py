@@ -87,19 +87,34 @@ class DeviceVolume:
         data = np.ascontiguousarray(v.data, dtype=np.float32)
         kind, stored = N.VOXEL_F32, data
         scalar_type = getattr(v, "scalar_type", "f32")
+        if raw is None:
+            raw = getattr(v, "raw", None)
         if raw is None and scalar_type in ("u8", "u16"):
-            scale, dt = (255.0, np.uint8) if scalar_type == "u8" else (65535.0, np.uint16)
-            cand = np.rint(data.astype(np.float64) * scale)
-            if cand.min() >= 0 and cand.max() <= scale:
-                cand = cand.astype(dt)
-                if np.array_equal(cand.astype(np.float32) / np.float32(scale), data):
-                    raw = cand
+            raw = _recover_raw(data, scalar_type)
         if raw is not None:
             raw = np.ascontiguousarray(raw)
             kind = {np.dtype(np.uint8): N.VOXEL_U8, np.dtype(np.uint16): N.VOXEL_U16}[raw.dtype]
             stored = raw.view(np.int16) if raw.dtype == np.uint16 else raw
         t = torch.from_numpy(stored).to(dev)
         return cls(t, kind, v.dims, v.box_lo, v.box_hi)
+
+
+def _recover_raw(data: np.ndarray, scalar_type: str, slab: int = 1 << 24):
+    """The u8/u16 integers behind a load_raw-normalised float32 grid, or None
+    if they do not reproduce it exactly; processed in slabs (bounded memory)."""
+    scale, dt = (255.0, np.uint8) if scalar_type == "u8" else (65535.0, np.uint16)
+    flat = data.reshape(-1)
+    out = np.empty(flat.shape, dtype=dt)
+    s32 = np.float32(scale)
+    for i in range(0, flat.size, slab):
+        chunk = flat[i:i + slab]
+        cand = np.rint(chunk.astype(np.float64) * scale)
+        if cand.min() < 0 or cand.max() > scale:
+            return None
+        out[i:i + slab] = cand
+        if not np.array_equal(out[i:i + slab].astype(np.float32) / s32, chunk):
+            return None
+    return out.reshape(data.shape)
 
 
 _VOLUME_CACHE: dict[int, tuple[weakref.ref, DeviceVolume]] = {}

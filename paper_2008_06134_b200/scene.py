@@ -119,8 +119,11 @@ class VolumeDataset:
         else:
             raise ValueError(f"unsupported raw dtype {raw.dtype}")
         nz, ny, nx = raw.shape
-        return cls(dims=(nx, ny, nz), spacing=tuple(spacing), scalar_type=kind,
-                   data=data.reshape(raw.shape), value_range=(lo, hi))
+        ds = cls(dims=(nx, ny, nz), spacing=tuple(spacing), scalar_type=kind,
+                 data=data.reshape(raw.shape), value_range=(lo, hi))
+        if kind in ("u8", "u16"):
+            ds.raw = raw  # the stored integers: the device copy keeps these (1-2 B per voxel)
+        return ds
 
     @property
     def voxel_size(self) -> np.ndarray:
