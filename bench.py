@@ -425,6 +425,16 @@ def run_ours(a, cfg, mode):
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["source"],
                 "algorithmic_bytes": d_bytes, "kernel_ms": d_ms,
                 "traffic": load_traffic(a.config, mode, dominant)}
+    # Secondary view of K2: the bytes its gathers pull through L1/L2 per sample
+    # (8 voxels + 2 16-byte texel quads per light lookup) against the SM-side
+    # L1 data bandwidth (128 B/clk/SM at the max SM clock). The march is bound
+    # there (and by load latency), not by HBM (DRAM ~2% busy, L1 hit ~95%).
+    lookups = {"none": 0, "sbrc_shadow": 1, "shell": 18, "cone": 8, "phong": 0, "extinction": 0}.get(mode, 0)
+    gathered = samples * (8 * vbytes + 32 * lookups)
+    l1_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+    l1 = {"bound": "l1", "kernel": "march", "achieved": gathered / (k2_ms * 1e-3) / 1e9, "peak": l1_peak,
+          "unit": "GB/s", "bytes_per_sample": 8 * vbytes + 32 * lookups}
+    l1["frac"] = l1["achieved"] / l1_peak
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -435,7 +445,7 @@ def run_ours(a, cfg, mode):
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
             "config": {"workload": f"config {a.config}: {cfg['name']}", "volume": f"{cfg['dims']}^3 "
                        + ("f32" if vbytes == 4 else ("u16" if vbytes == 2 else "u8")),
                        "image": [cfg["image"], cfg["image"]], "n_slices": cfg["n"],
@@ -450,6 +460,7 @@ def run_ours(a, cfg, mode):
                         "build_gbs": k1_bytes / (k1_ms * 1e-3) / 1e9, "march_gbs": k2_bytes / (k2_ms * 1e-3) / 1e9,
                         "build_gtexel_slices_s": cfg["n"] * cfg["res"] ** 2 / (k1_ms * 1e-3) / 1e9},
             "roofline": roofline,
+            "roofline_l1": l1,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 2 * a.steps,
@@ -540,9 +551,10 @@ def load_peaks():
     try:
         with open(p) as f:
             d = json.load(f)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
     except (OSError, KeyError, ValueError):
-        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
 
 
 def load_traffic(config, mode, kernel):

@@ -36,6 +36,9 @@
 #include <type_traits>
 
 // Compile-time variants (A/B'd in profiles/r01_notes.md).
+#ifndef SBRC_CONE_PREFETCH
+#define SBRC_CONE_PREFETCH 0  // 1: cone tap quads loaded one sample ahead
+#endif
 #ifndef SBRC_CONE_RING_SERIAL
 #define SBRC_CONE_RING_SERIAL 0  // 1: one cone ring's loads in flight at a time (fewer registers)
 #endif
@@ -753,6 +756,41 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
         if (cur_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, cur);
       }
 #endif
+#if SBRC_CONE_PREFETCH
+      // Cone taps software-pipelined one sample ahead: the 16 quad loads of
+      // sample j+1 are issued right after sample j's taps are consumed and
+      // fly during sample j+1's alpha path (interior fast path only; the
+      // weights are recomputed from the same float inputs at consumption).
+      constexpr bool CQ = SHADING == SBRC_SHADE_CONE && CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR;
+      constexpr int NQ = CQ ? 2 * CONE_A * NA : 1;
+      float4 cq[NQ];
+      auto cone_issue = [&](float jv, double tv) -> bool {
+        if constexpr (!CQ) {
+          return false;
+        } else {
+          const float tx = fmaf(jv, ftxs, ftx0), ty = fmaf(jv, ftys, fty0), li = fmaf(jv, flis, fli0);
+          const bool fast = (double)dperp * tv > 1e-12 && tx - reach_x >= 0.f && tx + reach_x < fast_x_hi &&
+                            ty - reach_y >= 0.f && ty + reach_y < fast_y_hi && li - (float)CONE_A >= 0.f &&
+                            li - 1.0f < fast_l_hi;
+          if (!fast) return false;
+#pragma unroll
+          for (int i = 1; i <= CONE_A; ++i) {
+            const float r = spacing_r * (float)i;
+            const unsigned kb = (unsigned)floor_f(li - (float)i).i * tex.qk;
+#pragma unroll
+            for (int j = 0; j < NA; ++j) {
+              const FloorF xl = floor_f(fmaf(r, wx[j], tx)), yl = floor_f(fmaf(r, wy[j], ty));
+              const unsigned off = kb + (unsigned)yl.i * tex.qy + (unsigned)xl.i;
+              const int q = 2 * ((i - 1) * NA + j);
+              cq[q] = __ldg(tex.q + off);
+              cq[q + 1] = __ldg(tex.q + off + tex.qy);
+            }
+          }
+          return true;
+        }
+      };
+      bool cq_ok = CQ ? cone_issue(0.0f, t) : false;
+#endif
       while (t < t_far && alpha < thresh) {
 #if SBRC_MARCH_PREFETCH
         const double tn = dadd(t, step);
@@ -845,6 +883,31 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
           } else {  // cone
             const bool degenerate = !((double)dperp * t > 1e-12);  // fallback plane_basis(L)[0] = axis_u
             float acc = 0.0f;
+#if SBRC_CONE_PREFETCH
+            if constexpr (CQ) {
+              if (cq_ok) {
+#pragma unroll
+                for (int i = 1; i <= CONE_A; ++i) {
+                  const float r = spacing_r * (float)i;
+                  const float lt = li - (float)i;
+                  const FloorF kl = floor_f(lt);
+                  float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+                  for (int j = 0; j < NA; ++j) {
+                    const float ttx = fmaf(r, wx[j], tx), tty = fmaf(r, wy[j], ty);
+                    const float fx = ttx - floor_f(ttx).f, fy = tty - floor_f(tty).f;
+                    const int q = 2 * ((i - 1) * NA + j);
+                    const float4 r0 = cq[q], r1 = cq[q + 1];
+                    v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
+                    v1 += lerpf(lerpf(r0.y, r0.w, fx), lerpf(r1.y, r1.w, fx), fy);
+                  }
+                  acc += lerpf(v0, v1, lt - kl.f);
+                }
+                scalar = acc * (1.0f / (float)(CONE_A * NA));
+              }
+            }
+            if (!(CQ && cq_ok)) {
+#endif
             const bool fast = CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR && !degenerate && tx - reach_x >= 0.f &&
                               tx + reach_x < fast_x_hi && ty - reach_y >= 0.f && ty + reach_y < fast_y_hi &&
                               li - (float)CONE_A >= 0.f && li - 1.0f < fast_l_hi;
@@ -897,6 +960,10 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
               }
               scalar = acc / (float)(P.cone_axis_samples * P.cone_angle_count);
             }
+#if SBRC_CONE_PREFETCH
+            }
+            if constexpr (CQ) cq_ok = cone_issue(jf + 1.0f, dadd(t, step));
+#endif
           }
           if (white) {
             fr = fg = fb = (double)fmaxf(scalar, 0.0f);
