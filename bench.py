@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--voxel", choices=("linear", "octet"), default="linear",
                     help="device layout of the volume: linear (x-fastest) or octets (8 corners per cell)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="N>1: disable overlapping the next frame's build with this frame's march")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also print a per-kernel detail line to stderr")
     a = ap.parse_args()
@@ -342,7 +344,7 @@ def run_ours(a, cfg, mode):
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2008_06134_b200 as sb
-    from paper_2008_06134_b200.frame import FrameRenderer
+    from paper_2008_06134_b200.frame import FramePipeline, FrameRenderer
 
     tf, cam, spec, settings = scene_objects(cfg, mode)
     t0 = time.perf_counter()
@@ -365,7 +367,13 @@ def run_ours(a, cfg, mode):
         dist.all_reduce(t)
         samples = int(t.item())
 
+    pipelined = world > 1 and a.build == "replicated" and not a.no_pipeline
+    pipe = FramePipeline(fr) if pipelined else None
+
     def one_step(ev=None):
+        if pipe is not None:  # build(f+1) on the build stream overlaps march(f)
+            pipe.step()
+            return
         if ev is not None:
             ev[0].record(stream)
         fr.build()
@@ -390,15 +398,33 @@ def run_ours(a, cfg, mode):
         start.record(stream)
         for i in range(a.steps):
             one_step(evs[i])
+        if pipe is not None:
+            pipe.drain()  # the build launched by the last step is inside the timed region
         end.record(stream)
         torch.cuda.synchronize()
         clocks.mark("t1")
     if world > 1:
         dist.barrier()
     total_ms = start.elapsed_time(end)
-    k1 = [e[0].elapsed_time(e[1]) for e in evs]
-    k2 = [e[1].elapsed_time(e[2]) for e in evs]
-    asm = [e[2].elapsed_time(e[3]) for e in evs]
+    if pipe is None:
+        k1 = [e[0].elapsed_time(e[1]) for e in evs]
+        k2 = [e[1].elapsed_time(e[2]) for e in evs]
+        asm = [e[2].elapsed_time(e[3]) for e in evs]
+    else:  # overlapped kernels: per-kernel times from a short serial run after the timed region
+        ser = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(5)]
+        fr.quads, fr._render_params = pipe.bufs[0], None
+        for e in ser:
+            e[0].record(stream)
+            fr.build()
+            e[1].record(stream)
+            fr.march(count_samples=False)
+            e[2].record(stream)
+            fr.assemble()
+            e[3].record(stream)
+        torch.cuda.synchronize()
+        k1 = [e[0].elapsed_time(e[1]) for e in ser]
+        k2 = [e[1].elapsed_time(e[2]) for e in ser]
+        asm = [e[2].elapsed_time(e[3]) for e in ser]
     stats = torch.tensor([total_ms, sum(k1) / len(k1), sum(k2) / len(k2), sum(asm) / len(asm)],
                          dtype=torch.float64, device=dev)
     if world > 1:
@@ -452,6 +478,7 @@ def run_ours(a, cfg, mode):
                        "slice_res": [cfg["res"], cfg["res"]], "step": cfg["step"], "shading_mode": mode,
                        "build": a.build if world > 1 else "single", "parallelism": f"image-tiles x{world}",
                        "assemble": fr.assemble_mode if world > 1 else "none",
+                       "frame_pipelining": "build(f+1) overlaps march(f)" if pipelined else "off",
                        "l2": "inputs larger than L2 (volume %d MiB, buffer %d MiB)" % (V >> 20, A >> 20)},
             "gsamples_per_s": samples / (k2_ms * 1e-3) / 1e9,
             "samples_per_frame": samples,

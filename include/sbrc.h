@@ -160,7 +160,12 @@ typedef struct sbrc_render_params {
    * i < n_peers — the full raster images of all ranks, mapped into this
    * process (CUDA IPC over NVLink). The caller then needs only a barrier. */
   float* peer_images[SBRC_MAX_PEERS];
-  int32_t n_peers, _pad3;
+  int32_t n_peers;
+  /* Optional dispatch order of the 2D block tiles (heavy-first scheduling):
+   * block b renders tile tile_order[b] (tile = ty * tiles_x + tx over the
+   * rank-local grid); NULL = natural order. n_tiles must equal the grid size. */
+  int32_t n_tiles;
+  const int32_t* tile_order;
   unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
 } sbrc_render_params;
 
@@ -255,6 +260,10 @@ int sbrc_ipc_free(void* ptr);
 int sbrc_ipc_handle(void* ptr, unsigned char handle[64]);
 int sbrc_ipc_open(const unsigned char handle[64], void** ptr);
 int sbrc_ipc_close(void* ptr);
+
+/* K2 grid for (width, height, band_rows, rank, world): grid[0..3] = tiles_x,
+ * tiles_y, tile width and height in pixels (for building tile_order tables). */
+int sbrc_march_grid(int width, int height, int band_rows, int rank, int world, int grid[4]);
 
 /* Number of rank-local image rows sbrc_render writes for (height, band_rows, rank, world). */
 int sbrc_local_rows(int height, int band_rows, int rank, int world);

@@ -36,6 +36,12 @@
 #include <type_traits>
 
 // Compile-time variants (A/B'd in profiles/r01_notes.md).
+#ifndef SBRC_MARCH_WARPS
+#define SBRC_MARCH_WARPS 8  // warps per K2 block
+#endif
+#ifndef SBRC_MARCH_WARPS_X
+#define SBRC_MARCH_WARPS_X 4  // of which along x
+#endif
 #ifndef SBRC_CONE_PREFETCH
 #define SBRC_CONE_PREFETCH 0  // 1: cone tap quads loaded one sample ahead
 #endif
@@ -563,7 +569,7 @@ struct ShellTap {
 #endif
 
 template <int SHADING, int LOOKUP, int VT, bool UNIT, int NSHELL, int CONE_A, int CONE_N>
-__global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const sbrc_render_params P) {
+__global__ void __launch_bounds__(32 * SBRC_MARCH_WARPS, SBRC_MARCH_MIN_BLOCKS) march_kernel(const sbrc_render_params P) {
   __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
@@ -621,9 +627,16 @@ __global__ void __launch_bounds__(256, SBRC_MARCH_MIN_BLOCKS) march_kernel(const
   // Pixel of this lane: each warp owns a TILE_W x (32/TILE_W) pixel tile, a
   // block 4 x 2 warp tiles.
   constexpr int TW = SBRC_TILE_W, TH = 32 / SBRC_TILE_W;
+  constexpr int WX = SBRC_MARCH_WARPS_X, WY = SBRC_MARCH_WARPS / SBRC_MARCH_WARPS_X;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int px = blockIdx.x * (4 * TW) + (warp & 3) * TW + (lane % TW);
-  const int lr = blockIdx.y * (2 * TH) + (warp >> 2) * TH + (lane / TW);  // rank-local row
+  int bx = blockIdx.x, by = blockIdx.y;
+  if (P.tile_order != nullptr) {  // heavy-first dispatch: this block renders tile tile_order[b]
+    const int t = __ldg(P.tile_order + blockIdx.y * gridDim.x + blockIdx.x);
+    bx = t % gridDim.x;
+    by = t / gridDim.x;
+  }
+  const int px = bx * (WX * TW) + (warp % WX) * TW + (lane % TW);
+  const int lr = by * (WY * TH) + (warp / WX) * TH + (lane / TW);  // rank-local row
   const int band = lr / P.band_rows;
   const int py = (P.rank + band * P.world) * P.band_rows + (lr - band * P.band_rows);
   const bool in_image = px < P.width && lr < P.local_rows;
@@ -1311,11 +1324,13 @@ void launch_build(const sbrc_build_params& p, cudaStream_t s) {
 
 template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN>
 void launch_march(const sbrc_render_params& p, cudaStream_t s) {
-  constexpr int BW = 4 * SBRC_TILE_W, BH = 2 * (32 / SBRC_TILE_W);
+  constexpr int WX = SBRC_MARCH_WARPS_X, WY = SBRC_MARCH_WARPS / SBRC_MARCH_WARPS_X;
+  constexpr int BW = WX * SBRC_TILE_W, BH = WY * (32 / SBRC_TILE_W);
   sbrc_render_params q = p;
   q.local_rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
   dim3 grid((p.width + BW - 1) / BW, (q.local_rows + BH - 1) / BH);
-  march_kernel<SH, LK, VT, UNIT, NS, CA, CN><<<grid, 256, 0, s>>>(q);
+  if (q.tile_order != nullptr && q.n_tiles != (int)(grid.x * grid.y)) q.tile_order = nullptr;  // stale table
+  march_kernel<SH, LK, VT, UNIT, NS, CA, CN><<<grid, 32 * SBRC_MARCH_WARPS, 0, s>>>(q);
 }
 
 template <int SH, int LK, int VT, bool UNIT>
@@ -1407,6 +1422,17 @@ int sbrc_ipc_open(const unsigned char handle[64], void** ptr) {
 }
 
 int sbrc_ipc_close(void* ptr) { return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? SBRC_OK : SBRC_ECUDA; }
+
+int sbrc_march_grid(int width, int height, int band_rows, int rank, int world, int* grid) {
+  if (grid == nullptr) return SBRC_EINVAL;
+  constexpr int WX = SBRC_MARCH_WARPS_X, WY = SBRC_MARCH_WARPS / SBRC_MARCH_WARPS_X;
+  constexpr int BW = WX * SBRC_TILE_W, BH = WY * (32 / SBRC_TILE_W);
+  grid[0] = (width + BW - 1) / BW;
+  grid[1] = (sbrc_local_rows(height, band_rows, rank, world) + BH - 1) / BH;
+  grid[2] = BW;
+  grid[3] = BH;
+  return SBRC_OK;
+}
 
 int sbrc_local_rows(int height, int band_rows, int rank, int world) {
   if (height < 1 || band_rows < 1 || world < 1 || rank < 0 || rank >= world) return 0;

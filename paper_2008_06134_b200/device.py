@@ -211,7 +211,7 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
                   quads_dev: torch.Tensor | None, light_color, voxel_size_max: float,
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
-                  peer_images=()) -> N.SbrcRenderParams:
+                  peer_images=(), tile_order: torch.Tensor | None = None) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469)."""
     mode = settings.shading_mode
     if mode not in N.SHADE:
@@ -270,5 +270,26 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     for i, ptr in enumerate(peer_images):
         p.peer_images[i] = int(ptr)
     p.n_peers = len(peer_images)
+    if tile_order is not None:
+        p.tile_order, p.n_tiles = tile_order.data_ptr(), int(tile_order.numel())
     p.sample_count = counter.data_ptr() if counter is not None else None
     return p
+
+
+_ORDER_CACHE: dict = {}
+
+
+def tile_order_for(settings, band_rows: int, rank: int, world: int, device) -> torch.Tensor:
+    """Device copy of the heavy-first dispatch table (schedule.heavy_first), cached per view."""
+    from .schedule import heavy_first
+    cam = settings.camera
+    key = (tuple(np.asarray(cam.position, np.float64)), tuple(np.asarray(cam.target, np.float64)),
+           tuple(np.asarray(cam.up, np.float64)), float(cam.fov_deg), tuple(settings.viewport), band_rows, rank,
+           world, str(device))
+    t = _ORDER_CACHE.get(key)
+    if t is None:
+        if len(_ORDER_CACHE) > 64:
+            _ORDER_CACHE.clear()
+        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world)).to(device)
+        _ORDER_CACHE[key] = t
+    return t

@@ -31,7 +31,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as N
-from .device import DeviceVolume, device_volume, f64_tensor, render_params, current_stream_handle
+from .device import DeviceVolume, device_volume, f64_tensor, render_params, current_stream_handle, tile_order_for
 from .lightbuffer import build_into, check_frame
 
 
@@ -107,7 +107,8 @@ class FrameRenderer:
     falls back to it (``assemble_mode``) if the images differ."""
 
     def __init__(self, volume, tf, light_cam, spec, settings, *, group=None, build: str = "replicated",
-                 band_rows: int = 8, compensation_n: float = 0.0, device=None, assemble: str = "nccl"):
+                 band_rows: int = 8, compensation_n: float = 0.0, device=None, assemble: str = "nccl",
+                 heavy_first: bool = True):
         check_frame(light_cam, spec)
         if build not in ("replicated", "sharded"):
             raise ValueError(f"build must be 'replicated' or 'sharded', got {build!r}")
@@ -120,6 +121,7 @@ class FrameRenderer:
         self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dvol = volume if isinstance(volume, DeviceVolume) else device_volume(volume, self.dev)
         self.tf, self.settings, self.build_mode = tf, settings, build
+        self.heavy_first = heavy_first
         self.band_rows, self.comp = band_rows, compensation_n
         self.lut = f64_tensor(tf.resolve(settings.step), self.dev)
         self.counter = torch.zeros(1, dtype=torch.int64, device=self.dev)
@@ -238,7 +240,9 @@ class FrameRenderer:
                 self.spec if buf_modes else None, self.quads if buf_modes else None,
                 self.cam.light_color, float(self.dvol.voxel_size.max()), None if p2p else self.chunk, self.counter,
                 band_rows=self.band_rows, rank=self.rank, world=self.world, voxel_size=self.dvol.voxel_size,
-                peer_images=self._peers if p2p else ())
+                peer_images=self._peers if p2p else (),
+                tile_order=tile_order_for(self.settings, self.band_rows, self.rank, self.world, self.dev)
+                if self.heavy_first else None)
         self._render_params.sample_count = self.counter.data_ptr() if count_samples else None
         N.check(N.lib.sbrc_render(self._render_params, current_stream_handle()), "sbrc_render")
 
@@ -278,3 +282,57 @@ class FrameRenderer:
     @property
     def buffer_bytes(self) -> int:
         return int(self.spec.n_slices) * int(self.cam.resolution[0]) * int(self.cam.resolution[1]) * 4
+
+
+class FramePipeline:
+    """Frames with the attenuation build of frame f+1 overlapping the march of
+    frame f (replicated build): two texel-quad buffers, a build stream and the
+    launching stream, ordered by events — build(f+1) waits until march(f-1)
+    has released its buffer, march(f) waits for build(f). Every frame still
+    runs its full build and march; the march leaves SMs idle in its tail (and
+    throughout when one GPU's share of the image is small), which the next
+    build fills."""
+
+    def __init__(self, fr: FrameRenderer):
+        if fr.shard is not None:
+            raise ValueError("pipelining needs the replicated build")
+        self.fr = fr
+        self.bufs = [fr.quads, torch.empty_like(fr.quads)]
+        self.build_stream = torch.cuda.Stream(fr.dev)
+        self.built = [torch.cuda.Event(), torch.cuda.Event()]
+        self.released = [torch.cuda.Event(), torch.cuda.Event()]
+        self.params = [None, None]
+        self.f = 0
+        self.pending = None  # buffer index whose build is in flight
+
+    def _launch_build(self, i: int) -> None:
+        fr = self.fr
+        with torch.cuda.stream(self.build_stream):
+            self.build_stream.wait_event(self.released[i])
+            build_into(fr.dvol, fr.alpha, fr.cam, fr.spec, fr.offsets, self.bufs[i], fr.comp)
+            self.built[i].record(self.build_stream)
+
+    def step(self, count_samples: bool = False) -> torch.Tensor:
+        fr, i = self.fr, self.f % 2
+        if self.pending is None:
+            self._launch_build(i)
+        self._launch_build(1 - i)  # next frame's stack, overlapping this march
+        self.pending = 1 - i
+        main = torch.cuda.current_stream(fr.dev)
+        main.wait_event(self.built[i])
+        if self.params[i] is None:
+            fr.quads, fr._render_params = self.bufs[i], None
+            fr.march(count_samples)
+            self.params[i] = fr._render_params
+        else:
+            fr._render_params = self.params[i]
+            fr.march(count_samples)
+        self.released[i].record(main)
+        img = fr.assemble()
+        self.f += 1
+        return img
+
+    def drain(self) -> None:
+        """Make the launching stream wait for the build in flight (end of a timed region)."""
+        if self.pending is not None:
+            torch.cuda.current_stream(self.fr.dev).wait_event(self.built[self.pending])

@@ -1,0 +1,55 @@
+"""Heavy-first tile scheduling for the march (K2).
+
+The march cannot finish before its slowest blocks — the tiles whose rays
+cross the most volume (hundreds of serial samples). With few blocks per SM
+(small images, or one rank's share of a multi-GPU frame) those tiles
+decide the kernel time if they start late. The block scheduler dispatches
+blocks roughly in index order, so the march reads a dispatch table
+(``tile_order``) that lists tiles by decreasing estimated cost: the
+geometric length of the rays inside the unit cube (ray_box_intersect,
+geometry.py:46-67), sampled at the tile's corners and centre.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from .scene import camera_frame
+
+
+def tile_cost(settings, band_rows: int = 8, rank: int = 0, world: int = 1) -> np.ndarray:
+    """(tiles_y, tiles_x) estimated cost (mean in-cube ray length) of the rank-local K2 tiles."""
+    w, h = int(settings.viewport[0]), int(settings.viewport[1])
+    tx, ty, bw, bh = N.march_grid(w, h, band_rows if world > 1 else 8, rank, world)
+    fr = camera_frame(settings.camera, settings.viewport)
+    eye = np.asarray(settings.camera.position, dtype=np.float64)
+    # sample pixels: corners and centre of every tile
+    offs = np.array([[0.0, 0.0], [bw - 1, 0.0], [0.0, bh - 1], [bw - 1, bh - 1], [bw / 2, bh / 2]])
+    gx, gy = np.meshgrid(np.arange(tx) * bw, np.arange(ty) * bh)
+    px = np.clip(gx[..., None] + offs[:, 0], 0, w - 1)
+    lr = gy[..., None] + offs[:, 1]
+    br = band_rows if world > 1 else 8
+    band = lr // br
+    py = np.clip((rank + band * world) * br + (lr - band * br), 0, h - 1)
+    ndc_x = ((px + 0.5) / w * 2.0 - 1.0) * fr["tan_half"] * fr["aspect"]
+    ndc_y = (1.0 - (py + 0.5) / h * 2.0) * fr["tan_half"]
+    d = fr["forward"] + ndc_x[..., None] * fr["right"] + ndc_y[..., None] * fr["up2"]
+    d = d / np.linalg.norm(d, axis=-1, keepdims=True)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / d
+        a = (0.0 - eye) * inv
+        b = (1.0 - eye) * inv
+    flat = d == 0.0
+    inside = (eye >= 0.0) & (eye <= 1.0)
+    a = np.where(flat, np.where(inside, -np.inf, np.inf), a)
+    b = np.where(flat, np.where(inside, np.inf, -np.inf), b)
+    t_in = np.maximum(np.minimum(a, b).max(axis=-1), 0.0)
+    t_out = np.maximum(a, b).min(axis=-1)
+    return np.where(t_out > t_in, t_out - t_in, 0.0).mean(axis=-1)
+
+
+def heavy_first(settings, band_rows: int = 8, rank: int = 0, world: int = 1) -> np.ndarray:
+    """int32 dispatch table: tile indices (ty * tiles_x + tx) by decreasing cost."""
+    cost = tile_cost(settings, band_rows, rank, world).reshape(-1)
+    return np.argsort(-cost, kind="stable").astype(np.int32)

@@ -34,6 +34,13 @@ def _worker(rank, world, port, q):
         mode = fr.assemble_mode
         img = fr.frame().cpu().numpy()
         err = float(np.abs(img - g["image_cone_linear"]).max())
+        # pipelined frames (next build overlapping this march) give the same image
+        from paper_2008_06134_b200.frame import FramePipeline
+        pipe = FramePipeline(fr)
+        for _ in range(3):
+            out = pipe.step()
+        pipe.drain()
+        err = max(err, float(np.abs(out.cpu().numpy() - g["image_cone_linear"]).max()))
         fr.close()
         q.put((rank, mode, err, None))
     except Exception as exc:  # report instead of hanging the parent
