@@ -70,8 +70,6 @@ def parse():
     ap.add_argument("--assemble", choices=("p2p", "nccl"), default="p2p",
                     help="N>1 image assembly: fused peer-memory stores from the march kernel (self-checked, "
                          "falls back to NCCL) or NCCL all-gather")
-    ap.add_argument("--voxel", choices=("linear", "octet"), default="linear",
-                    help="device layout of the volume: linear (x-fastest) or octets (8 corners per cell)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="N>1: disable overlapping the next frame's build with this frame's march")
@@ -349,8 +347,6 @@ def run_ours(a, cfg, mode):
     tf, cam, spec, settings = scene_objects(cfg, mode)
     t0 = time.perf_counter()
     dvol, host_vol = device_volume_for(cfg, dev)
-    if a.voxel == "octet":
-        dvol = dvol.octets()
     torch.cuda.synchronize()
     vol_gen_s = time.perf_counter() - t0
     fr = FrameRenderer(dvol, tf, cam, spec, settings, build=a.build if world > 1 else "replicated",
@@ -439,7 +435,7 @@ def run_ours(a, cfg, mode):
         e2e = e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev)
 
     # ---- roofline of the dominant kernel
-    vbytes = {0: 4, 1: 1, 2: 2}[dvol.voxel_type % 4]  # algorithmic V counts the source bytes per voxel
+    vbytes = {0: 4, 1: 1, 2: 2}[dvol.voxel_type]  # algorithmic V counts the stored bytes per voxel
     V, A, I = algorithmic_bytes(cfg, vbytes, world)
     k1_bytes = V + (A if (world == 1 or a.build == "replicated") else A // world)
     k2_bytes = (V + A + I // world) if mode != "none" else (V + I // world)

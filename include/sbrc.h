@@ -54,12 +54,7 @@ typedef enum sbrc_status {
 typedef enum sbrc_voxel_type {
   SBRC_VOXEL_F32 = 0, /* already-normalised float32 (volume.py:147-149)          */
   SBRC_VOXEL_U8 = 1,  /* raw u8, normalised at fetch as (float)x / 255.0f (volume.py:143-144) */
-  SBRC_VOXEL_U16 = 2, /* raw u16, normalised at fetch as (float)x / 65535.0f (volume.py:145-146) */
-  /* octet layouts (sbrc_pack_octets): cell (cx,cy,cz) in [0,n]^3 stores the 8
-   * clamped corners of the trilinear cell with low corner (cx-1,cy-1,cz-1) */
-  SBRC_VOXEL_F32_OCT = 4,
-  SBRC_VOXEL_U8_OCT = 5,
-  SBRC_VOXEL_U16_OCT = 6
+  SBRC_VOXEL_U16 = 2  /* raw u16, normalised at fetch as (float)x / 65535.0f (volume.py:145-146) */
 } sbrc_voxel_type;
 
 typedef enum sbrc_shading {
@@ -187,10 +182,6 @@ int sbrc_volume_check(const sbrc_volume* v);
  * data[i] = fl32(fl32(data[i] - lo) / range), range = fl32(hi - lo) > 0 —
  * numpy's float32 arithmetic, so bit-identical. */
 int sbrc_normalize_f32(float* data, int64_t n, float lo, float range, void* stream);
-
-/* K0: repack a linear F32/U8/U16 volume into its octet layout; dst holds
- * (nx+1)(ny+1)(nz+1) cells of 8 voxels (32/8/16 bytes). */
-int sbrc_pack_octets(const sbrc_volume* src, void* dst, void* stream);
 
 /* K1: attenuation build (lightbuffer.py:144-199). */
 int sbrc_build(const sbrc_build_params* p, void* stream);

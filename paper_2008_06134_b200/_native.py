@@ -23,13 +23,12 @@ MAX_PEERS = 8
 
 OK, EINVAL, ECONFIG, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4
 VOXEL_F32, VOXEL_U8, VOXEL_U16 = 0, 1, 2
-VOXEL_OCT = 4  # + base type: F32_OCT 4, U8_OCT 5, U16_OCT 6
 SHADE = {"none": 0, "sbrc_shadow": 1, "shell": 2, "cone": 3, "phong": 4, "extinction": 5}
 LOOKUP = {"linear": 0, "nearest": 1}
 
 #: every symbol include/sbrc.h declares
 EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume_check",
-           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_pack_octets", "sbrc_shadow_oracle", "sbrc_light_factor",
+           "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_shadow_oracle", "sbrc_light_factor",
            "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_ipc_alloc", "sbrc_ipc_free", "sbrc_ipc_handle",
            "sbrc_ipc_open", "sbrc_ipc_close", "sbrc_march_grid", "sbrc_local_rows")
 
@@ -111,7 +110,6 @@ def _load() -> C.CDLL:
     lib.sbrc_half_angle.argtypes = [C.POINTER(SbrcHalfAngleParams), C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(C.c_int), C.c_void_p]
     lib.sbrc_normalize_f32.argtypes = [C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_void_p]
-    lib.sbrc_pack_octets.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p]
     lib.sbrc_shadow_oracle.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_double, C.c_void_p, C.c_void_p]
     lib.sbrc_pack_quads.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,

@@ -15,7 +15,10 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "sbrc.cu")
+CSRC = os.path.join(HERE, "csrc")
+#: translation units: the C ABI + one per shading mode (K2 instantiations compile in parallel)
+SOURCES = ["sbrc.cu"] + [f"march_{m}.cu" for m in ("cone", "shell", "shadow", "none", "phong", "extinction")]
+SRC = os.path.join(CSRC, "sbrc.cu")
 OUT = os.path.join(HERE, "_sbrc.so")
 
 NVCC_FLAGS = [
@@ -33,21 +36,37 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(verbose: bool = False, force: bool = False, out: str = OUT, defines=()) -> str:
-    """Compile; ``defines`` (e.g. ["SBRC_MARCH_MIN_BLOCKS=3"]) and ``out`` build experiment variants."""
-    deps = [SRC, os.path.join(ROOT, "include", "sbrc.h")]
+def build(verbose: bool = False, force: bool = False, out: str = OUT, defines=(), jobs: int | None = None) -> str:
+    """Compile every translation unit (in parallel) and link ``out``; ``defines``
+    (e.g. ["SBRC_MARCH_MIN_BLOCKS=3"]) and ``out`` build experiment variants."""
+    import concurrent.futures as cf
+    import tempfile
+    srcs = [os.path.join(CSRC, f) for f in SOURCES]
+    deps = srcs + [os.path.join(CSRC, "sbrc_common.cuh"), os.path.join(ROOT, "include", "sbrc.h")]
     if not force and os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
         return out
-    OUT_ = out
-    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], *(["-Xptxas", "-v"] if verbose else []),
-           "-o", OUT_ + ".tmp", SRC]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr}")
-    if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(OUT_ + ".tmp", OUT_)
-    return OUT_
+    tmp = tempfile.mkdtemp(prefix="sbrc_build_")
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    extra = [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else [])
+
+    def compile_one(src):
+        obj = os.path.join(tmp, os.path.basename(src) + ".o")
+        res = subprocess.run([nvcc(), *compile_flags, *extra, "-c", "-o", obj, src], capture_output=True, text=True)
+        return src, obj, res
+
+    with cf.ThreadPoolExecutor(max_workers=jobs or min(len(srcs), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    for src, obj, res in results:
+        if verbose:
+            sys.stderr.write(res.stderr)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {os.path.basename(src)} ({res.returncode}):\n{res.stderr}")
+    link = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out + ".tmp",
+                           *[obj for _, obj, _ in results]], capture_output=True, text=True)
+    if link.returncode != 0:
+        raise RuntimeError(f"nvcc link failed ({link.returncode}):\n{link.stderr}")
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

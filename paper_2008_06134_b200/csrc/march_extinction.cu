@@ -1,0 +1,4 @@
+// K2 instantiations for shading mode "extinction" (see sbrc_common.cuh).
+#include "sbrc_common.cuh"
+
+void sbrc_march_extinction(const sbrc_render_params& p, cudaStream_t s) { launch_march_lookup<SBRC_SHADE_EXTINCTION>(p, s); }

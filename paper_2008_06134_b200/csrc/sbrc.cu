@@ -1,276 +1,11 @@
-// sbrc.cu — B200 (sm_100a) kernels for slice-based ray casting with volume
-// illumination (arXiv 2008.06134), behind the C ABI in include/sbrc.h.
-//
-//   K1 build_kernel  <- slicecast.lightbuffer.build_attenuation_buffer
-//                       (/root/reference/pkg/src/slicecast/lightbuffer.py:144-199)
-//   K2 march_kernel  <- slicecast.raycaster.render / _march_rays / _make_shader
-//                       (raycaster.py:376-469) with lookup_light_scalar_many
-//                       (lightbuffer.py:256-287), _shell_scalar (:239-250),
-//                       _cone_scalar (:266-300), _factor_from_intensity (:197-201)
-//   pack_quads       <- repacks an externally built (n, H, W) stack
-//
-// Numerics. Everything that decides WHICH samples exist and
-// the alpha that drives early termination — cube coverage of a texel-slice
-// point, ray entry/exit, the float64 march counter `t += step`, the
-// inside-cube test, trilinear reconstruction, the TF lookup and the alpha
-// accumulation — is float64 with numpy's operation order and no FMA
-// contraction (explicit __dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn), so it is
-// bit-identical to the reference. The light factor (buffer lookups for
-// sbrc/shell/cone) is a continuous function of position and runs in fp32;
-// it only scales colour. No hardware texture filtering: its 8-bit weights
-// would break 1e-3.
-//
-// Performance notes (profiles/). The march is issue-bound,
-// not HBM-bound (L1 hit rate ~98%): the design minimises instructions per
-// sample — texel quads turn a two-layer bilinear lookup into two 16-byte
-// loads, offsets are 32-bit, edge clamping is folded into saturated
-// weights, the trilinear fetch has an unclamped interior fast path, and the
-// default cone (2 x 4) and shell (3 shells) kernels are unrolled.
+// sbrc.cu — the C ABI of include/sbrc.h: K1 (attenuation build), the
+// point-wise light factor, shadow oracle, half-angle baseline, raw-volume
+// normalisation, IPC helpers, and K2 dispatch to march_<mode>.cu.
+// Kernel documentation and the numerics contract: sbrc_common.cuh.
 
-#include "../../include/sbrc.h"
-
-#include <cuda_runtime.h>
-#include <stdint.h>
-#include <string.h>
-
-#include <type_traits>
-
-// Compile-time variants (A/B'd in profiles/r01_notes.md).
-#ifndef SBRC_MARCH_WARPS
-#define SBRC_MARCH_WARPS 8  // warps per K2 block
-#endif
-#ifndef SBRC_MARCH_WARPS_X
-#define SBRC_MARCH_WARPS_X 4  // of which along x
-#endif
-#ifndef SBRC_CONE_PREFETCH
-#define SBRC_CONE_PREFETCH 0  // 1: cone tap quads loaded one sample ahead
-#endif
-#ifndef SBRC_CONE_RING_SERIAL
-#define SBRC_CONE_RING_SERIAL 0  // 1: one cone ring's loads in flight at a time (fewer registers)
-#endif
-#ifndef SBRC_BUILD_UNROLL
-#define SBRC_BUILD_UNROLL 2  // slices whose gathers are in flight together in K1
-#endif
-#ifndef SBRC_BUILD_SHUFFLE
-#define SBRC_BUILD_SHUFFLE 1  // one 16-byte store per quad (warp shuffle for the x+1 neighbour)
-#endif
+#include "sbrc_common.cuh"
 
 namespace {
-
-// ---------------------------------------------------------------- float64
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
-__device__ __forceinline__ double dclip01(double x) { return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x); }
-__device__ __forceinline__ bool in01(double x) { return x >= 0.0 && x <= 1.0; }
-
-// Exact floors without the conversion pipe (F2I/FRND/F2F issue at a quarter
-// of the FMA rate and were a third of the march's instructions): adding
-// 1.5*2^52 (resp. 1.5*2^23) with round-toward-minus-infinity lands exactly on
-// floor(x) + magic for |x| < 2^51 (2^22); the low word is the integer.
-struct FloorD {
-  double f;
-  int i;
-};
-__device__ __forceinline__ FloorD floor_d(double x) {
-  const double m = __dadd_rd(x, 6755399441055744.0);
-  return FloorD{__dsub_rn(m, 6755399441055744.0), __double2loint(m)};
-}
-struct FloorF {
-  float f;
-  int i;
-};
-__device__ __forceinline__ FloorF floor_f(float x) {
-  const float m = __fadd_rd(x, 12582912.0f);
-  return FloorF{__fsub_rn(m, 12582912.0f), __float_as_int(m) - 0x4B400000};
-}
-
-// ---------------------------------------------------------------- volume
-// Voxel fetch with load_raw's normalisation (volume.py:143-149): u8/u16 are
-// kept raw in HBM and normalised at fetch. u8 uses a 256-entry table of
-// __fdiv_rn(x, 255.f) (held as double); u16 computes (float)((double)x / 65535) through a
-// double product, which rounds to the same float as the IEEE float32
-// division because x/65535 is never within 2^-40 of a float midpoint.
-// Both are bit-identical to numpy's `astype(float32) / 255.0` etc.
-template <int VT> struct Voxel;
-template <> struct Voxel<SBRC_VOXEL_F32> {
-  using T = float;
-  static constexpr bool oct = false;
-  static __device__ __forceinline__ double cvt(float x, const float*) { return (double)x; }
-};
-template <> struct Voxel<SBRC_VOXEL_U8> {
-  using T = unsigned char;
-  static constexpr bool oct = false;
-  static __device__ __forceinline__ double cvt(unsigned char x, const float* tab) {
-    return reinterpret_cast<const double*>(tab)[x];
-  }
-};
-template <> struct Voxel<SBRC_VOXEL_U16> {
-  using T = unsigned short;
-  static constexpr bool oct = false;
-  static __device__ __forceinline__ double cvt(unsigned short x, const float*) {
-    return (double)__double2float_rn(dmul((double)x, 1.0 / 65535.0));
-  }
-};
-// Octet layouts: cell (cx, cy, cz) in [0, n]^3 holds the 8 corner values of
-// the trilinear cell whose low corner is (cx-1, cy-1, cz-1), with the
-// reference's clamping i0 = clip(lo), i1 = clip(lo+1) baked in, ordered
-// d000 d100 d010 d110 d001 d101 d011 d111: one cell = one or two 16-byte loads.
-template <int BASE> struct OctetOf : Voxel<BASE> {
-  static constexpr bool oct = true;
-  static constexpr int base = BASE;
-};
-template <> struct Voxel<SBRC_VOXEL_F32_OCT> : OctetOf<SBRC_VOXEL_F32> {};
-template <> struct Voxel<SBRC_VOXEL_U8_OCT> : OctetOf<SBRC_VOXEL_U8> {};
-template <> struct Voxel<SBRC_VOXEL_U16_OCT> : OctetOf<SBRC_VOXEL_U16> {};
-
-template <typename T>
-__device__ __forceinline__ void load_octet(const void* data, unsigned cell, T r[8]) {
-  if constexpr (sizeof(T) == 4) {
-    const float4* o = reinterpret_cast<const float4*>(data) + 2 * (size_t)cell;
-    const float4 a = __ldg(o), b = __ldg(o + 1);
-    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
-  } else if constexpr (sizeof(T) == 2) {
-    const uint4 a = __ldg(reinterpret_cast<const uint4*>(data) + cell);
-    const unsigned w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      r[2 * i] = (T)(w[i] & 0xffffu);
-      r[2 * i + 1] = (T)(w[i] >> 16);
-    }
-  } else {
-    const uint2 a = __ldg(reinterpret_cast<const uint2*>(data) + cell);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      r[i] = (T)((a.x >> (8 * i)) & 0xffu);
-      r[4 + i] = (T)((a.y >> (8 * i)) & 0xffu);
-    }
-  }
-}
-
-// Cell-centred trilinear reconstruction, clamp-to-edge, 0 outside the unit
-// cube: sample_trilinear_many (volume.py:161-194), same op order. Split in
-// cell_fetch (indices, fractions, the 8 gathers) and cell_combine (the
-// float64 lerps) so callers can issue the gathers of the next slice/sample
-// before combining the current one. The voxel index is 32-bit (validated:
-// nx*ny*nz < 2^32). UNIT: the volume box is the unit cube (box_lo = 0,
-// box_hi = 1: every cubic dataset), where local = (p - 0)/1 = p exactly and
-// the clip is a no-op inside the cube.
-template <int VT>
-struct Cell {
-  typename Voxel<VT>::T r[8];  // d000 d100 d010 d110 d001 d101 d011 d111
-  double f[3];
-};
-
-template <int VT, bool UNIT>
-__device__ __forceinline__ void cell_fetch(const sbrc_volume& v, double px, double py, double pz, Cell<VT>& cl) {
-  using T = typename Voxel<VT>::T;
-  const double p[3] = {px, py, pz};
-  const int dims[3] = {v.nx, v.ny, v.nz};
-  int lo[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    double local = p[c];
-    if (!UNIT) local = dclip01(ddiv(dsub(p[c], v.box_lo[c]), v.box_ext[c]));
-    const double g = dsub(dmul(local, (double)dims[c]), 0.5);
-    const FloorD fl = floor_d(g);
-    cl.f[c] = dsub(g, fl.f);
-    lo[c] = fl.i;
-  }
-  if constexpr (Voxel<VT>::oct) {
-    // lo in [-1, n-1] (local in [0,1]); the octet grid is (n+1)^3
-    const unsigned cell = (unsigned)(lo[0] + 1) +
-                          (unsigned)(v.nx + 1) * ((unsigned)(lo[1] + 1) + (unsigned)(v.ny + 1) * (unsigned)(lo[2] + 1));
-    load_octet<T>(v.data, cell, cl.r);
-    return;
-  } else {
-  const T* base = reinterpret_cast<const T*>(v.data);
-  const unsigned nx = (unsigned)v.nx, nxy = (unsigned)v.nx * (unsigned)v.ny;
-  if ((unsigned)lo[0] < (unsigned)(v.nx - 1) && (unsigned)lo[1] < (unsigned)(v.ny - 1) &&
-      (unsigned)lo[2] < (unsigned)(v.nz - 1)) {
-    // interior: the 2x2x2 cell without clamping
-    const T* c = base + ((unsigned)lo[0] + nx * (unsigned)lo[1] + nxy * (unsigned)lo[2]);
-    const T* cy = c + nx;
-    const T* cz = c + nxy;
-    const T* cyz = cz + nx;
-    cl.r[0] = __ldg(c); cl.r[1] = __ldg(c + 1); cl.r[2] = __ldg(cy); cl.r[3] = __ldg(cy + 1);
-    cl.r[4] = __ldg(cz); cl.r[5] = __ldg(cz + 1); cl.r[6] = __ldg(cyz); cl.r[7] = __ldg(cyz + 1);
-  } else {
-    // faces: i0 = clip(lo), i1 = clip(lo + 1) (volume.py:180-182)
-    unsigned a[3], b[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      a[c] = (unsigned)min(max(lo[c], 0), dims[c] - 1);
-      b[c] = (unsigned)min(max(lo[c] + 1, 0), dims[c] - 1);
-    }
-    const unsigned z0 = a[2] * nxy, z1 = b[2] * nxy, y0 = a[1] * nx, y1 = b[1] * nx;
-    cl.r[0] = __ldg(base + (z0 + y0 + a[0])); cl.r[1] = __ldg(base + (z0 + y0 + b[0]));
-    cl.r[2] = __ldg(base + (z0 + y1 + a[0])); cl.r[3] = __ldg(base + (z0 + y1 + b[0]));
-    cl.r[4] = __ldg(base + (z1 + y0 + a[0])); cl.r[5] = __ldg(base + (z1 + y0 + b[0]));
-    cl.r[6] = __ldg(base + (z1 + y1 + a[0])); cl.r[7] = __ldg(base + (z1 + y1 + b[0]));
-  }
-  }
-}
-
-template <int VT>
-__device__ __forceinline__ double cell_combine(const Cell<VT>& cl, const float* u8tab) {
-  using V = Voxel<VT>;
-  const double* f = cl.f;
-  const double gx = dsub(1.0, f[0]), gy = dsub(1.0, f[1]), gz = dsub(1.0, f[2]);
-  const double c00 = dadd(dmul(V::cvt(cl.r[0], u8tab), gx), dmul(V::cvt(cl.r[1], u8tab), f[0]));
-  const double c10 = dadd(dmul(V::cvt(cl.r[2], u8tab), gx), dmul(V::cvt(cl.r[3], u8tab), f[0]));
-  const double c01 = dadd(dmul(V::cvt(cl.r[4], u8tab), gx), dmul(V::cvt(cl.r[5], u8tab), f[0]));
-  const double c11 = dadd(dmul(V::cvt(cl.r[6], u8tab), gx), dmul(V::cvt(cl.r[7], u8tab), f[0]));
-  const double c0 = dadd(dmul(c00, gy), dmul(c10, f[1]));
-  const double c1 = dadd(dmul(c01, gy), dmul(c11, f[1]));
-  return dadd(dmul(c0, gz), dmul(c1, f[2]));
-}
-
-__device__ __forceinline__ bool in_cube(double px, double py, double pz) { return in01(px) && in01(py) && in01(pz); }
-
-template <int VT, bool UNIT>
-__device__ __forceinline__ double trilinear64(const sbrc_volume& v, const float* u8tab, double px, double py,
-                                              double pz) {
-  if (!in_cube(px, py, pz)) return 0.0;
-  Cell<VT> cl;
-  cell_fetch<VT, UNIT>(v, px, py, pz, cl);
-  return cell_combine<VT>(cl, u8tab);
-}
-
-// u8 normalisation table: tab[x] = (double)((float)x / 255.0f), IEEE division.
-__device__ __forceinline__ void fill_u8_table(double* tab) {
-  for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < 256; i += blockDim.x * blockDim.y)
-    tab[i] = (double)__fdiv_rn((float)i, 255.0f);
-}
-
-// LUT position: t = clip(s,0,1)*255, i0 = floor(t) (truncation, s >= 0),
-// i1 = min(i0+1, 255), f = t - i0 (transfer.py:93-100, lightbuffer.py:188-191).
-struct LutPos {
-  int i0, i1;
-  double f, g;
-};
-__device__ __forceinline__ LutPos lut_pos(double s) {
-  LutPos r;
-  const double t = dmul(dclip01(s), 255.0);
-  const FloorD fl = floor_d(t);
-  r.i0 = fl.i;
-  r.i1 = min(r.i0 + 1, SBRC_LUT_SIZE - 1);
-  r.f = dsub(t, fl.f);
-  r.g = dsub(1.0, r.f);
-  return r;
-}
-
-// ---------------------------------------------------------------- texel quads
-// Quad (k, y, x) = (I[k][y][x], I[k+][y][x], I[k][y][x+], I[k+][y][x+]).
-// Writing texel x's pair (I[k], I[k+]) fills .xy of quad x and .zw of quad
-// x-1 (and .zw of quad x at the right edge, where x+ = x).
-__device__ __forceinline__ void emit_pair(float4* row, int x, int w, float a, float b) {
-  float2* r2 = reinterpret_cast<float2*>(row);
-  r2[2 * x] = make_float2(a, b);
-  if (x > 0) r2[2 * x - 1] = make_float2(a, b);
-  if (x == w - 1) r2[2 * x + 1] = make_float2(a, b);
-}
 
 // ---------------------------------------------------------------- K1 build
 // One thread per light texel; the slice recurrence runs in registers
@@ -404,622 +139,6 @@ __global__ void __launch_bounds__(256) pack_quads_kernel(const float* __restrict
   emit_pair(row + (size_t)(n - 1) * (size_t)qk, x, w, prev, prev);
 }
 
-// ---------------------------------------------------------------- rays
-// ray_box_intersect (geometry.py:46-67) for one ray: slab test against the
-// unit cube with the reference's parallel-ray handling; t_enter = max(t_near, 0).
-__device__ __forceinline__ bool box_hit(const double o[3], const double d[3], double& t_enter, double& t_far) {
-  double t_near = -INFINITY;
-  t_far = INFINITY;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    double lo, hi;
-    if (d[c] == 0.0) {
-      const bool inside = in01(o[c]);
-      lo = inside ? -INFINITY : INFINITY;
-      hi = inside ? INFINITY : -INFINITY;
-    } else {
-      const double inv = ddiv(1.0, d[c]);
-      lo = dmul(dsub(0.0, o[c]), inv);
-      hi = dmul(dsub(1.0, o[c]), inv);
-    }
-    t_near = fmax(t_near, fmin(lo, hi));
-    t_far = fmin(t_far, fmax(lo, hi));
-  }
-  t_enter = fmax(t_near, 0.0);
-  return t_far > t_enter;
-}
-
-// ALPHA_MAX = 1 - 1e-6 (raycaster.py:34)
-#define SBRC_ALPHA_MAX (1.0 - 1e-6)
-
-// Straight march from p toward the light (raycaster.py:312-353): EXT returns
-// sum(-log1p(-min(a, ALPHA_MAX))) (_extinction_scalar), otherwise
-// prod(1 - min(a, ALPHA_MAX)) (_shadow_oracle_scalar). Float64, reference op
-// order; only log1p's last ulp can differ from glibc's.
-template <int VT, bool UNIT, bool EXT>
-__device__ double light_march(const sbrc_volume& v, const double* alut, const float* u8tab, const double p[3],
-                              const double tl[3], double step) {
-  double t_enter, t_far;
-  if (!box_hit(p, tl, t_enter, t_far)) return EXT ? 0.0 : 1.0;
-  double acc = EXT ? 0.0 : 1.0;
-  for (double t = dadd(t_enter, 0.5 * step); t < t_far; t = dadd(t, step)) {
-    const double s = trilinear64<VT, UNIT>(v, u8tab, dadd(p[0], dmul(t, tl[0])), dadd(p[1], dmul(t, tl[1])),
-                                           dadd(p[2], dmul(t, tl[2])));
-    const LutPos q = lut_pos(s);
-    const double a = fmin(dadd(dmul(alut[q.i0], q.g), dmul(alut[q.i1], q.f)), SBRC_ALPHA_MAX);
-    if (EXT) acc = dadd(acc, -log1p(-a));
-    else acc = dmul(acc, dsub(1.0, a));
-  }
-  return acc;
-}
-
-// _phong_scalar (raycaster.py:204-220) with gradient_many (volume.py:201-220):
-// central differences with probes clamped to the cube, divided by the actual
-// probe separation; the lit test |g| > 1e-12 sees the same float64 gradient.
-template <int VT, bool UNIT>
-__device__ double phong_scalar(const sbrc_render_params& P, const float* u8tab, const double p[3]) {
-  double g[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    double hi[3] = {dclip01(p[0]), dclip01(p[1]), dclip01(p[2])};
-    double lo[3] = {hi[0], hi[1], hi[2]};
-    hi[a] = dclip01(dadd(p[a], P.voxel_size[a]));
-    lo[a] = dclip01(dsub(p[a], P.voxel_size[a]));
-    double sep = dsub(hi[a], lo[a]);
-    if (sep == 0.0) sep = 1.0;
-    g[a] = ddiv(dsub(trilinear64<VT, UNIT>(P.volume, u8tab, hi[0], hi[1], hi[2]),
-                     trilinear64<VT, UNIT>(P.volume, u8tab, lo[0], lo[1], lo[2])), sep);
-  }
-  const double norm = __dsqrt_rn(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
-  const double ambient = P.phong[0];
-  if (!(norm > 1e-12)) return ambient;
-  double n[3], view[3];
-  double vn = 0.0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    n[c] = ddiv(-g[c], norm);
-    view[c] = dsub(P.eye[c], p[c]);
-    vn += view[c] * view[c];
-  }
-  vn = sqrt(vn);
-  double ndl = 0.0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) ndl += n[c] * -P.scene_light_dir[c];
-  ndl = fmax(0.0, ndl);
-  double rdv = 0.0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) rdv += (2.0 * ndl * n[c] + P.scene_light_dir[c]) * (view[c] / vn);
-  rdv = fmax(0.0, rdv);
-  return ambient + (P.phong[1] * ndl + P.phong[2] * pow(rdv, P.phong[3]));
-}
-
-// ---------------------------------------------------------------- K2 march
-// Light-space lookup state. Texel coordinates tx = u*W - 0.5, ty = v*H - 0.5
-// and the layer coordinate li = idx - 0.5 (lightbuffer.py:241-242, :279).
-struct QuadTex {
-  const float4* q;
-  unsigned qk, qy, qy1;  // layer / row strides in quads; qy1 = row step to y+1 (0 if H == 1)
-  float txmax, tymax;    // footprint: u in [0,1]  <=>  tx in [-0.5, W-0.5]
-  float xa_max, ya_max;  // max(W-2, 0), max(H-2, 0)
-  float li_max, ka_max;  // n-1, max(n-2, 0)
-};
-
-__device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b, fmaf(-t, a, a)); }
-
-// lookup_light_scalar_many at one point (lightbuffer.py:256-287): 1 outside
-// the footprint (:268-269); linear: bilinear in the two layers bracketing
-// plane-centred coordinate li, blended (:277-285); nearest: one layer
-// (:274-276). Index clamping (clip(x0,0,W-1), clip(x0+1,0,W-1)) is replaced
-// by clamping the cell to [0, W-2] and saturating the weight, which selects
-// the same texel values.
-template <int LOOKUP>
-__device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float ty, float li_raw) {
-  // li_raw: idx - 0.5 for linear lookups, idx for nearest
-  if (!(tx >= -0.5f && tx <= t.txmax && ty >= -0.5f && ty <= t.tymax)) return 1.0f;
-  const float xa = fminf(fmaxf(floor_f(tx).f, 0.0f), t.xa_max);
-  const float ya = fminf(fmaxf(floor_f(ty).f, 0.0f), t.ya_max);
-  const float fx = __saturatef(tx - xa), fy = __saturatef(ty - ya);
-  float ka, f;
-  if (LOOKUP == SBRC_LOOKUP_NEAREST) {
-    // k = floor(clip(idx, 0, n-1)) (:275); for nearest lookups li_raw is idx
-    ka = floor_f(fminf(fmaxf(li_raw, 0.0f), t.li_max)).f;
-    f = 0.0f;
-  } else {
-    const float li = fminf(fmaxf(li_raw, 0.0f), t.li_max);
-    ka = fminf(floor_f(li).f, t.ka_max);
-    f = li - ka;
-  }
-  const unsigned off = (unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa;
-  const float4 r0 = __ldg(t.q + off);
-  const float4 r1 = __ldg(t.q + off + t.qy1);
-  const float a0 = lerpf(r0.x, r0.z, fx), a1 = lerpf(r1.x, r1.z, fx);  // layer ka, rows y, y+1
-  const float v0 = lerpf(a0, a1, fy);
-  if (LOOKUP == SBRC_LOOKUP_NEAREST) return v0;
-  const float b0 = lerpf(r0.y, r0.w, fx), b1 = lerpf(r1.y, r1.w, fx);  // layer ka+1
-  return lerpf(v0, lerpf(b0, b1, fy), f);
-}
-
-// Interior tap: the caller guarantees 0 <= tx < W-1 and 0 <= ty < H-1, so the
-// footprint test passes and no clamp of light_lookup is active; the two
-// layers of quad layer offset `kbase` are accumulated separately into v0/v1
-// and blended once per layer pair by the caller.
-__device__ __forceinline__ void interior_tap(const QuadTex& t, unsigned kbase, float tx, float ty, float& v0,
-                                             float& v1) {
-  const FloorF xl = floor_f(tx), yl = floor_f(ty);
-  const float fx = tx - xl.f, fy = ty - yl.f;
-  const unsigned off = kbase + (unsigned)yl.i * t.qy + (unsigned)xl.i;
-  const float4 r0 = __ldg(t.q + off);
-  const float4 r1 = __ldg(t.q + off + t.qy);
-  v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
-  v1 += lerpf(lerpf(r0.y, r0.w, fx), lerpf(r1.y, r1.w, fx), fy);
-}
-
-struct ShellTap {
-  float dtx, dty, dli, w;  // texel-space offset of +radius along one world axis; shell weight
-};
-
-#ifndef SBRC_TILE_W
-#define SBRC_TILE_W 8  // warp pixel tile width (8 x 4)
-#endif
-#ifndef SBRC_MARCH_PREFETCH
-#define SBRC_MARCH_PREFETCH 1
-#endif
-#ifndef SBRC_MARCH_MIN_BLOCKS
-#define SBRC_MARCH_MIN_BLOCKS 2  // 128 registers, no spills: 16 warps per SM (A/B in profiles/r01_notes.md)
-#endif
-
-template <int SHADING, int LOOKUP, int VT, bool UNIT, int NSHELL, int CONE_A, int CONE_N>
-__global__ void __launch_bounds__(32 * SBRC_MARCH_WARPS, SBRC_MARCH_MIN_BLOCKS) march_kernel(const sbrc_render_params P) {
-  __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
-  __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
-  __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
-  __shared__ double u8tab[256];
-  __shared__ double alut[SHADING == SBRC_SHADE_EXTINCTION ? SBRC_LUT_SIZE : 1];
-  for (int i = threadIdx.x; i < SBRC_LUT_SIZE * 2; i += blockDim.x)
-    lut[i] = reinterpret_cast<const double2*>(P.lut_rgba)[i];
-  if (SHADING == SBRC_SHADE_EXTINCTION)
-    for (int i = threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x) alut[i] = P.lut_rgba[4 * i + 3];
-  if (std::is_same<typename Voxel<VT>::T, unsigned char>::value) fill_u8_table(u8tab);
-
-  const sbrc_light_frame& LF = P.light;
-  // Light space (world_to_light_uv_many :202-212, slice_index_many slicing.py:101-105):
-  // tx = ((p.au - u0)/(u1-u0))*W - 0.5, ty likewise, li = n (p.L - d_min)/(d_max - d_min) - 0.5.
-  const double sx = (double)LF.width / (LF.u_range[1] - LF.u_range[0]);
-  const double sy = (double)LF.height / (LF.v_range[1] - LF.v_range[0]);
-  const double si = (double)LF.n_slices / (LF.d_max - LF.d_min);
-  // Interior reach of the scattering kernel in texel / layer units: a sample
-  // whose light-space position is at least this far inside the buffer has all
-  // its taps inside too, and takes the clamp-free fast path.
-  float reach_x = 0.f, reach_y = 0.f, reach_l = 0.f;
-  if (SHADING == SBRC_SHADE_SHELL) {
-    // p +- r e_a maps to (tx, ty, li) +- r (au[a] sx, av[a] sy, L[a] si).
-    for (int i = threadIdx.x; i < P.shell_count * 3; i += blockDim.x) {
-      const int s = i / 3, a = i % 3;
-      const double r = P.shell_radius[s];
-      shell_taps[i] = ShellTap{(float)(r * LF.axis_u[a] * sx), (float)(r * LF.axis_v[a] * sy),
-                               (float)(r * LF.light_dir[a] * si), (float)P.shell_weight[s]};
-    }
-    double rmax = 0.0;
-    for (int s = 0; s < P.shell_count; ++s) rmax = fmax(rmax, P.shell_radius[s]);
-    double mu = 0.0, mv = 0.0, ml = 0.0;
-    for (int a = 0; a < 3; ++a) {
-      mu = fmax(mu, fabs(LF.axis_u[a]));
-      mv = fmax(mv, fabs(LF.axis_v[a]));
-      ml = fmax(ml, fabs(LF.light_dir[a]));
-    }
-    reach_x = (float)(rmax * mu * sx * 1.001 + 1e-3);
-    reach_y = (float)(rmax * mv * sy * 1.001 + 1e-3);
-    reach_l = (float)(rmax * ml * si * 1.001 + 1e-3);
-  }
-  if (SHADING == SBRC_SHADE_CONE) {
-    const double rr = P.cone_ring * ((LF.d_max - LF.d_min) / LF.n_slices) * P.cone_axis_samples;
-    reach_x = (float)(rr * sx * 1.001 + 1e-3);
-    reach_y = (float)(rr * sy * 1.001 + 1e-3);
-  }
-  const float fast_x_hi = (float)(LF.width - 1), fast_y_hi = (float)(LF.height - 1);
-  const float fast_l_hi = (float)(LF.n_slices - 1);
-  if (SHADING == SBRC_SHADE_CONE) {
-    for (int i = threadIdx.x; i < P.cone_angle_count; i += blockDim.x)
-      cone_cs[i] = make_float2((float)P.cone_cos[i], (float)P.cone_sin[i]);
-  }
-  __syncthreads();
-
-  // Pixel of this lane: each warp owns a TILE_W x (32/TILE_W) pixel tile, a
-  // block 4 x 2 warp tiles.
-  constexpr int TW = SBRC_TILE_W, TH = 32 / SBRC_TILE_W;
-  constexpr int WX = SBRC_MARCH_WARPS_X, WY = SBRC_MARCH_WARPS / SBRC_MARCH_WARPS_X;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int bx = blockIdx.x, by = blockIdx.y;
-  if (P.tile_order != nullptr) {  // heavy-first dispatch: this block renders tile tile_order[b]
-    const int t = __ldg(P.tile_order + blockIdx.y * gridDim.x + blockIdx.x);
-    bx = t % gridDim.x;
-    by = t / gridDim.x;
-  }
-  const int px = bx * (WX * TW) + (warp % WX) * TW + (lane % TW);
-  const int lr = by * (WY * TH) + (warp / WX) * TH + (lane / TW);  // rank-local row
-  const int band = lr / P.band_rows;
-  const int py = (P.rank + band * P.world) * P.band_rows + (lr - band * P.band_rows);
-  const bool in_image = px < P.width && lr < P.local_rows;
-  const bool valid = in_image && py < P.height;
-
-  unsigned int samples = 0;
-  float4 result = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (valid) {
-    // ---- Camera.rays (raycaster.py:53-68), numpy op order, float64.
-    const double ndc_x = dmul(dmul(dsub(dmul(ddiv(dadd((double)px, 0.5), (double)P.width), 2.0), 1.0),
-                                   P.tan_half), P.aspect);
-    const double ndc_y = dmul(dsub(1.0, dmul(ddiv(dadd((double)py, 0.5), (double)P.height), 2.0)), P.tan_half);
-    double d[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) d[c] = dadd(dadd(P.forward[c], dmul(ndc_x, P.right[c])), dmul(ndc_y, P.up2[c]));
-    const double nrm = __dsqrt_rn(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
-#pragma unroll
-    for (int c = 0; c < 3; ++c) d[c] = ddiv(d[c], nrm);
-
-    // ---- ray_box_intersect (geometry.py:46-67) against the unit cube.
-    double t_near = -INFINITY, t_far = INFINITY;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double lo, hi;
-      if (d[c] == 0.0) {
-        const bool inside = in01(P.eye[c]);
-        lo = inside ? -INFINITY : INFINITY;
-        hi = inside ? INFINITY : -INFINITY;
-      } else {
-        const double inv = ddiv(1.0, d[c]);
-        lo = dmul(dsub(0.0, P.eye[c]), inv);
-        hi = dmul(dsub(1.0, P.eye[c]), inv);
-      }
-      t_near = fmax(t_near, fmin(lo, hi));
-      t_far = fmin(t_far, fmax(lo, hi));
-    }
-    const double t_enter = fmax(t_near, 0.0);
-
-    if (t_far > t_enter) {
-      QuadTex tex;
-      // Light-space coordinates are affine in t along the ray: c(t) = c0 + t*cd.
-      double tx0 = 0, txd = 0, ty0 = 0, tyd = 0, li0 = 0, lid = 0;
-      float cbu = 1.0f, cbv = 0.0f, dperp = 0.0f;
-      float fr_c = 1.f, fg_c = 1.f, fb_c = 1.f, ir = 1.f, ig = 1.f, ib = 1.f;
-      constexpr bool BUFFERED = SHADING == SBRC_SHADE_SHADOW || SHADING == SBRC_SHADE_SHELL || SHADING == SBRC_SHADE_CONE;
-      if (BUFFERED) {
-        tex.q = reinterpret_cast<const float4*>(P.quads);
-        tex.qk = (unsigned)P.quad_layer_stride;
-        tex.qy = (unsigned)P.quad_row_stride;
-        tex.qy1 = LF.height > 1 ? tex.qy : 0u;
-        tex.txmax = (float)LF.width - 0.5f;
-        tex.tymax = (float)LF.height - 0.5f;
-        tex.xa_max = (float)max(LF.width - 2, 0);
-        tex.ya_max = (float)max(LF.height - 2, 0);
-        tex.li_max = (float)(LF.n_slices - 1);
-        tex.ka_max = (float)max(LF.n_slices - 2, 0);
-        double eu = 0, ev = 0, el = 0, du_ = 0, dv_ = 0, dl_ = 0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          eu += P.eye[c] * LF.axis_u[c];
-          ev += P.eye[c] * LF.axis_v[c];
-          el += P.eye[c] * LF.light_dir[c];
-          du_ += d[c] * LF.axis_u[c];
-          dv_ += d[c] * LF.axis_v[c];
-          dl_ += d[c] * LF.light_dir[c];
-        }
-        tx0 = (eu - LF.u_range[0]) * sx - 0.5;
-        txd = du_ * sx;
-        ty0 = (ev - LF.v_range[0]) * sy - 0.5;
-        tyd = dv_ * sy;
-        // linear lookups use the plane-centred li = idx - 0.5; nearest uses idx itself
-        li0 = (el - LF.d_min) * si - (LOOKUP == SBRC_LOOKUP_NEAREST ? 0.0 : 0.5);
-        lid = dl_ * si;
-        if (SHADING == SBRC_SHADE_CONE) {
-          // Ring basis: normalize(e - (e.L)L) with e = eye - p = -t d, so it is
-          // -d_perp/|d_perp| for the whole ray (raycaster.py:276-282); its
-          // in-plane coordinates are (-du_, -dv_)/|d_perp|.
-          const double pn = sqrt(du_ * du_ + dv_ * dv_);
-          dperp = (float)pn;
-          if (pn > 0.0) {
-            cbu = (float)(-du_ / pn);
-            cbv = (float)(-dv_ / pn);
-          }
-        }
-        // _factor_from_intensity (raycaster.py:197-201): max(s*c, floor)/c, 1 where c == 0
-        fr_c = P.light_color[0];
-        fg_c = P.light_color[1];
-        fb_c = P.light_color[2];
-        ir = fr_c > 0.f ? 1.0f / fr_c : 0.f;
-        ig = fg_c > 0.f ? 1.0f / fg_c : 0.f;
-        ib = fb_c > 0.f ? 1.0f / fb_c : 0.f;
-      }
-      // white light without ambient floor: factor = max(s, 0) on every channel
-      const bool white = fr_c == 1.f && fg_c == 1.f && fb_c == 1.f && P.ambient_floor == 0.f;
-      // Cone ring geometry per ray (texel units): tap (i, j) sits at
-      // (tx + r_i*wx_j, ty + r_i*wy_j, li - i), r_i = ring * i * spacing.
-      constexpr int NA = CONE_N > 0 ? CONE_N : 1;
-      float wx[NA], wy[NA];
-      const float spacing_r = (float)(P.cone_ring * ((LF.d_max - LF.d_min) / LF.n_slices));
-      float bu_fb = cbu, bv_fb = cbv;
-      if (SHADING == SBRC_SHADE_CONE && CONE_N > 0) {
-#pragma unroll
-        for (int j = 0; j < NA; ++j) {
-          const float c = (float)P.cone_cos[j], s = (float)P.cone_sin[j];
-          wx[j] = (float)sx * (cbu * c - cbv * s);
-          wy[j] = (float)sy * (cbv * c + cbu * s);
-        }
-      }
-      const double step = P.step, thresh = P.et_alpha;
-      double t = dadd(t_enter, 0.5 * step);
-      // fp32 light-space centre: c(t) ~= c(t0) + j * step * dc/dt with a float
-      // sample counter j (exact below 2^24), so no conversion per sample; the
-      // float64 t stays the sample-position authority.
-      const float ftx0 = (float)fma(t, txd, tx0), fty0 = (float)fma(t, tyd, ty0), fli0 = (float)fma(t, lid, li0);
-      const float ftxs = (float)(txd * step), ftys = (float)(tyd * step), flis = (float)(lid * step);
-      float jf = 0.0f;
-      double cr = 0.0, cg = 0.0, cb = 0.0, alpha = 0.0;
-      // Front-to-back march (raycaster.py:428-439): the live test precedes
-      // each sample, so the sample that crosses the threshold is kept.
-#if SBRC_MARCH_PREFETCH
-      // the voxel cell of sample j+1 is gathered while sample j is shaded
-      // (harmless past the exit: outside the cube nothing is fetched)
-      Cell<VT> cur;
-      bool cur_in;
-      {
-        const double qx = dadd(P.eye[0], dmul(t, d[0]));
-        const double qy = dadd(P.eye[1], dmul(t, d[1]));
-        const double qz = dadd(P.eye[2], dmul(t, d[2]));
-        cur_in = in_cube(qx, qy, qz);
-        if (cur_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, cur);
-      }
-#endif
-#if SBRC_CONE_PREFETCH
-      // Cone taps software-pipelined one sample ahead: the 16 quad loads of
-      // sample j+1 are issued right after sample j's taps are consumed and
-      // fly during sample j+1's alpha path (interior fast path only; the
-      // weights are recomputed from the same float inputs at consumption).
-      constexpr bool CQ = SHADING == SBRC_SHADE_CONE && CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR;
-      constexpr int NQ = CQ ? 2 * CONE_A * NA : 1;
-      float4 cq[NQ];
-      auto cone_issue = [&](float jv, double tv) -> bool {
-        if constexpr (!CQ) {
-          return false;
-        } else {
-          const float tx = fmaf(jv, ftxs, ftx0), ty = fmaf(jv, ftys, fty0), li = fmaf(jv, flis, fli0);
-          const bool fast = (double)dperp * tv > 1e-12 && tx - reach_x >= 0.f && tx + reach_x < fast_x_hi &&
-                            ty - reach_y >= 0.f && ty + reach_y < fast_y_hi && li - (float)CONE_A >= 0.f &&
-                            li - 1.0f < fast_l_hi;
-          if (!fast) return false;
-#pragma unroll
-          for (int i = 1; i <= CONE_A; ++i) {
-            const float r = spacing_r * (float)i;
-            const unsigned kb = (unsigned)floor_f(li - (float)i).i * tex.qk;
-#pragma unroll
-            for (int j = 0; j < NA; ++j) {
-              const FloorF xl = floor_f(fmaf(r, wx[j], tx)), yl = floor_f(fmaf(r, wy[j], ty));
-              const unsigned off = kb + (unsigned)yl.i * tex.qy + (unsigned)xl.i;
-              const int q = 2 * ((i - 1) * NA + j);
-              cq[q] = __ldg(tex.q + off);
-              cq[q + 1] = __ldg(tex.q + off + tex.qy);
-            }
-          }
-          return true;
-        }
-      };
-      bool cq_ok = CQ ? cone_issue(0.0f, t) : false;
-#endif
-      while (t < t_far && alpha < thresh) {
-#if SBRC_MARCH_PREFETCH
-        const double tn = dadd(t, step);
-        Cell<VT> nxt;
-        bool nxt_in;
-        {
-          const double qx = dadd(P.eye[0], dmul(tn, d[0]));
-          const double qy = dadd(P.eye[1], dmul(tn, d[1]));
-          const double qz = dadd(P.eye[2], dmul(tn, d[2]));
-          nxt_in = in_cube(qx, qy, qz);
-          if (nxt_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, nxt);
-        }
-        const double s = cur_in ? cell_combine<VT>(cur, reinterpret_cast<const float*>(u8tab)) : 0.0;
-#else
-        const double qx = dadd(P.eye[0], dmul(t, d[0]));
-        const double qy = dadd(P.eye[1], dmul(t, d[1]));
-        const double qz = dadd(P.eye[2], dmul(t, d[2]));
-        const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), qx, qy, qz);
-#endif
-        const LutPos q = lut_pos(s);
-        const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
-        const double2 b_rg = lut[2 * q.i1], b_ba = lut[2 * q.i1 + 1];
-        const double sr = dadd(dmul(a_rg.x, q.g), dmul(b_rg.x, q.f));
-        const double sg = dadd(dmul(a_rg.y, q.g), dmul(b_rg.y, q.f));
-        const double sb = dadd(dmul(a_ba.x, q.g), dmul(b_ba.x, q.f));
-        const double sa = dadd(dmul(a_ba.y, q.g), dmul(b_ba.y, q.f));
-
-        double fr = 1.0, fg = 1.0, fb = 1.0;
-        if (SHADING == SBRC_SHADE_PHONG || SHADING == SBRC_SHADE_EXTINCTION) {
-          const double p[3] = {dadd(P.eye[0], dmul(t, d[0])), dadd(P.eye[1], dmul(t, d[1])),
-                               dadd(P.eye[2], dmul(t, d[2]))};
-          double f;
-          if (SHADING == SBRC_SHADE_PHONG) {
-            f = phong_scalar<VT, UNIT>(P, reinterpret_cast<const float*>(u8tab), p);  // raycaster.py:385-388
-          } else {  // raycaster.py:389-394: max(exp(-tau), floor), alpha LUT at settings.step
-            const double tl[3] = {-P.scene_light_dir[0], -P.scene_light_dir[1], -P.scene_light_dir[2]};
-            const double tau = light_march<VT, UNIT, true>(P.volume, alut, reinterpret_cast<const float*>(u8tab),
-                                                          p, tl, step);
-            f = fmax(exp(-tau), (double)P.ambient_floor);
-          }
-          fr = fg = fb = f;
-        } else if (SHADING != SBRC_SHADE_NONE) {
-          const float tx = fmaf(jf, ftxs, ftx0);
-          const float ty = fmaf(jf, ftys, fty0);
-          const float li = fmaf(jf, flis, fli0);
-          float scalar;
-          if (SHADING == SBRC_SHADE_SHADOW) {
-            scalar = light_lookup<LOOKUP>(tex, tx, ty, li);
-          } else if (SHADING == SBRC_SHADE_SHELL) {
-            float acc = 0.0f;
-            const int nsh = NSHELL > 0 ? NSHELL : P.shell_count;
-            const bool fast = LOOKUP == SBRC_LOOKUP_LINEAR && tx - reach_x >= 0.f && tx + reach_x < fast_x_hi &&
-                              ty - reach_y >= 0.f && ty + reach_y < fast_y_hi && li - reach_l >= 0.f &&
-                              li + reach_l < fast_l_hi;
-            if (fast) {
-#pragma unroll
-              for (int sh = 0; sh < (NSHELL > 0 ? NSHELL : SBRC_MAX_SHELLS); ++sh) {
-                if (NSHELL == 0 && sh >= nsh) break;
-                float shell = 0.0f;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                  const ShellTap tp = shell_taps[sh * 3 + a];
-#pragma unroll
-                  for (int sg = 0; sg < 2; ++sg) {
-                    const float sgn = sg ? -1.0f : 1.0f;
-                    const float lt = fmaf(sgn, tp.dli, li);
-                    const FloorF kl = floor_f(lt);
-                    float v0 = 0.f, v1 = 0.f;
-                    interior_tap(tex, (unsigned)kl.i * tex.qk, fmaf(sgn, tp.dtx, tx), fmaf(sgn, tp.dty, ty), v0, v1);
-                    shell += lerpf(v0, v1, lt - kl.f);
-                  }
-                }
-                acc += shell_taps[sh * 3].w * shell / 6.0f;
-              }
-            } else {
-#pragma unroll
-              for (int sh = 0; sh < (NSHELL > 0 ? NSHELL : SBRC_MAX_SHELLS); ++sh) {
-                if (NSHELL == 0 && sh >= nsh) break;
-                float shell = 0.0f;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                  const ShellTap tp = shell_taps[sh * 3 + a];
-                  shell += light_lookup<LOOKUP>(tex, tx + tp.dtx, ty + tp.dty, li + tp.dli);
-                  shell += light_lookup<LOOKUP>(tex, tx - tp.dtx, ty - tp.dty, li - tp.dli);
-                }
-                acc += shell_taps[sh * 3].w * shell / 6.0f;
-              }
-            }
-            scalar = acc;
-          } else {  // cone
-            const bool degenerate = !((double)dperp * t > 1e-12);  // fallback plane_basis(L)[0] = axis_u
-            float acc = 0.0f;
-#if SBRC_CONE_PREFETCH
-            if constexpr (CQ) {
-              if (cq_ok) {
-#pragma unroll
-                for (int i = 1; i <= CONE_A; ++i) {
-                  const float r = spacing_r * (float)i;
-                  const float lt = li - (float)i;
-                  const FloorF kl = floor_f(lt);
-                  float v0 = 0.f, v1 = 0.f;
-#pragma unroll
-                  for (int j = 0; j < NA; ++j) {
-                    const float ttx = fmaf(r, wx[j], tx), tty = fmaf(r, wy[j], ty);
-                    const float fx = ttx - floor_f(ttx).f, fy = tty - floor_f(tty).f;
-                    const int q = 2 * ((i - 1) * NA + j);
-                    const float4 r0 = cq[q], r1 = cq[q + 1];
-                    v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
-                    v1 += lerpf(lerpf(r0.y, r0.w, fx), lerpf(r1.y, r1.w, fx), fy);
-                  }
-                  acc += lerpf(v0, v1, lt - kl.f);
-                }
-                scalar = acc * (1.0f / (float)(CONE_A * NA));
-              }
-            }
-            if (!(CQ && cq_ok)) {
-#endif
-            const bool fast = CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR && !degenerate && tx - reach_x >= 0.f &&
-                              tx + reach_x < fast_x_hi && ty - reach_y >= 0.f && ty + reach_y < fast_y_hi &&
-                              li - (float)CONE_A >= 0.f && li - 1.0f < fast_l_hi;
-            if (fast) {
-              // every tap inside the buffer: one layer pair per ring, blended once
-#if SBRC_CONE_RING_SERIAL
-#pragma unroll 1
-#else
-#pragma unroll
-#endif
-              for (int i = 1; i <= CONE_A; ++i) {
-                const float r = spacing_r * (float)i;
-                const float lt = li - (float)i;
-                const FloorF kl = floor_f(lt);
-                const unsigned kb = (unsigned)kl.i * tex.qk;
-                float v0 = 0.f, v1 = 0.f;
-#pragma unroll
-                for (int j = 0; j < NA; ++j) interior_tap(tex, kb, fmaf(r, wx[j], tx), fmaf(r, wy[j], ty), v0, v1);
-                acc += lerpf(v0, v1, lt - kl.f);
-              }
-              scalar = acc * (1.0f / (float)(CONE_A * NA));
-            } else if (CONE_N > 0) {
-#pragma unroll
-              for (int i = 1; i <= CONE_A; ++i) {
-                const float r = spacing_r * (float)i;
-                const float ki = li - (float)i;
-#pragma unroll
-                for (int j = 0; j < NA; ++j) {
-                  float ox = r * wx[j], oy = r * wy[j];
-                  if (degenerate) {
-                    const float c = cone_cs[j].x, sn = cone_cs[j].y;
-                    ox = r * (float)sx * c;
-                    oy = r * (float)sy * sn;
-                  }
-                  acc += light_lookup<LOOKUP>(tex, tx + ox, ty + oy, ki);
-                }
-              }
-              scalar = acc * (1.0f / (float)(CONE_A * NA));
-            } else {
-              const float bu = degenerate ? 1.0f : bu_fb, bv = degenerate ? 0.0f : bv_fb;
-              for (int i = 1; i <= P.cone_axis_samples; ++i) {
-                const float r = spacing_r * (float)i;
-                const float ki = li - (float)i;
-                for (int j = 0; j < P.cone_angle_count; ++j) {
-                  const float2 cs = cone_cs[j];
-                  const float ox = r * (float)sx * (bu * cs.x - bv * cs.y);
-                  const float oy = r * (float)sy * (bv * cs.x + bu * cs.y);
-                  acc += light_lookup<LOOKUP>(tex, tx + ox, ty + oy, ki);
-                }
-              }
-              scalar = acc / (float)(P.cone_axis_samples * P.cone_angle_count);
-            }
-#if SBRC_CONE_PREFETCH
-            }
-            if constexpr (CQ) cq_ok = cone_issue(jf + 1.0f, dadd(t, step));
-#endif
-          }
-          if (white) {
-            fr = fg = fb = (double)fmaxf(scalar, 0.0f);
-          } else {
-            fr = fr_c > 0.f ? (double)(fmaxf(scalar * fr_c, P.ambient_floor) * ir) : 1.0;
-            fg = fg_c > 0.f ? (double)(fmaxf(scalar * fg_c, P.ambient_floor) * ig) : 1.0;
-            fb = fb_c > 0.f ? (double)(fmaxf(scalar * fb_c, P.ambient_floor) * ib) : 1.0;
-          }
-        }
-        // C += (1-a)*rgb*factor; a += (1-a)*a_src (raycaster.py:436-438)
-        const double one_m = dsub(1.0, alpha);
-        cr = dadd(cr, dmul(dmul(one_m, sr), fr));
-        cg = dadd(cg, dmul(dmul(one_m, sg), fg));
-        cb = dadd(cb, dmul(dmul(one_m, sb), fb));
-        alpha = dadd(alpha, dmul(one_m, sa));
-#if SBRC_MARCH_PREFETCH
-        t = tn;
-        cur = nxt;
-        cur_in = nxt_in;
-#else
-        t = dadd(t, step);
-#endif
-        jf += 1.0f;
-        ++samples;
-      }
-      result = make_float4((float)cr, (float)cg, (float)cb, (float)alpha);
-    }
-  }
-  if (in_image) {  // background (and padding rows of a partial last band) is transparent black
-    if (P.image != nullptr) reinterpret_cast<float4*>(P.image)[(size_t)lr * P.width + px] = result;
-    // fused assembly: the pixel goes straight into every rank's raster image
-    // (peer memory over NVLink); a barrier after the kernel completes the frame
-    if (valid)
-      for (int i = 0; i < P.n_peers; ++i)
-        reinterpret_cast<float4*>(P.peer_images[i])[(size_t)py * P.width + px] = result;
-  }
-  if (P.n_peers > 0) __threadfence_system();
-  if (P.sample_count != nullptr) {
-    const unsigned int tot = __reduce_add_sync(0xffffffffu, samples);
-    if (lane == 0 && tot) atomicAdd(P.sample_count, (unsigned long long)tot);
-  }
-}
-
 // GPU shadow_oracle_many (raycaster.py:356-366): one thread per point.
 template <int VT, bool UNIT>
 __global__ void __launch_bounds__(256) shadow_oracle_kernel(const sbrc_volume V, const double* __restrict__ alpha_lut,
@@ -1035,27 +154,6 @@ __global__ void __launch_bounds__(256) shadow_oracle_kernel(const sbrc_volume V,
   const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
   const double tl[3] = {tl0, tl1, tl2};
   out[i] = light_march<VT, UNIT, false>(V, alut, reinterpret_cast<const float*>(u8tab), p, tl, step);
-}
-
-// K0 octet repack: one thread per octet cell (cx, cy, cz) in [0, n]^3.
-template <typename T>
-__global__ void __launch_bounds__(256) pack_octets_kernel(const T* __restrict__ src, int nx, int ny, int nz, T* dst) {
-  const long long cells = (long long)(nx + 1) * (ny + 1) * (nz + 1);
-  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
-       c += (long long)gridDim.x * blockDim.x) {
-    const int cx = (int)(c % (nx + 1));
-    const int cy = (int)((c / (nx + 1)) % (ny + 1));
-    const int cz = (int)(c / ((long long)(nx + 1) * (ny + 1)));
-    const int x0 = max(cx - 1, 0), x1 = min(cx, nx - 1);
-    const int y0 = max(cy - 1, 0), y1 = min(cy, ny - 1);
-    const int z0 = max(cz - 1, 0), z1 = min(cz, nz - 1);
-    const size_t sy = (size_t)nx, sz = (size_t)nx * ny;
-    T* o = dst + 8 * (size_t)c;
-    o[0] = src[z0 * sz + y0 * sy + x0]; o[1] = src[z0 * sz + y0 * sy + x1];
-    o[2] = src[z0 * sz + y1 * sy + x0]; o[3] = src[z0 * sz + y1 * sy + x1];
-    o[4] = src[z1 * sz + y0 * sy + x0]; o[5] = src[z1 * sz + y0 * sy + x1];
-    o[6] = src[z1 * sz + y1 * sy + x0]; o[7] = src[z1 * sz + y1 * sy + x1];
-  }
 }
 
 // Light factor at arbitrary world points: lookup_light_scalar_many
@@ -1279,37 +377,6 @@ void has_passes(const sbrc_half_angle_params& p, int k0, int k1, cudaStream_t s)
   }
 }
 
-// ---------------------------------------------------------------- dispatch
-bool volume_ok(const sbrc_volume& v) {
-  if (v.data == nullptr) return false;
-  if (v.nx < 2 || v.ny < 2 || v.nz < 2) return false;  // volume.py:80-81
-  if ((unsigned long long)v.nx * v.ny * v.nz >= (1ull << 32)) return false;  // 32-bit voxel offsets
-  if (v.voxel_type < SBRC_VOXEL_F32 || v.voxel_type > SBRC_VOXEL_U16_OCT) return false;
-  if (v.voxel_type >= SBRC_VOXEL_F32_OCT && (unsigned long long)(v.nx + 1) * (v.ny + 1) * (v.nz + 1) >= (1ull << 32))
-    return false;
-  for (int c = 0; c < 3; ++c)
-    if (!(v.box_ext[c] > 0.0)) return false;
-  return true;
-}
-
-bool light_ok(const sbrc_light_frame& L) {
-  return L.width >= 1 && L.height >= 1 && L.n_slices >= 1 && L.d_max > L.d_min &&
-         L.u_range[1] > L.u_range[0] && L.v_range[1] > L.v_range[0];
-}
-
-// Largest quad offset must fit 32 bits (K2 addresses quads with 32-bit offsets).
-bool quads_ok(const sbrc_light_frame& L, int64_t qk, int64_t qy) {
-  if (qk < 1 || qy < L.width) return false;
-  const long long last = (long long)(L.n_slices - 1) * qk + (long long)(L.height - 1) * qy + L.width;
-  return last < (1ll << 32);
-}
-
-bool unit_box(const sbrc_volume& v) {
-  for (int c = 0; c < 3; ++c)
-    if (v.box_lo[c] != 0.0 || v.box_ext[c] != 1.0) return false;
-  return true;
-}
-
 template <int VT>
 void launch_build(const sbrc_build_params& p, cudaStream_t s) {
   dim3 block(32, 8);
@@ -1320,52 +387,6 @@ void launch_build(const sbrc_build_params& p, cudaStream_t s) {
 #endif
   if (unit_box(p.volume)) build_kernel<VT, true><<<grid, block, 0, s>>>(p);
   else build_kernel<VT, false><<<grid, block, 0, s>>>(p);
-}
-
-template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN>
-void launch_march(const sbrc_render_params& p, cudaStream_t s) {
-  constexpr int WX = SBRC_MARCH_WARPS_X, WY = SBRC_MARCH_WARPS / SBRC_MARCH_WARPS_X;
-  constexpr int BW = WX * SBRC_TILE_W, BH = WY * (32 / SBRC_TILE_W);
-  sbrc_render_params q = p;
-  q.local_rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
-  dim3 grid((p.width + BW - 1) / BW, (q.local_rows + BH - 1) / BH);
-  if (q.tile_order != nullptr && q.n_tiles != (int)(grid.x * grid.y)) q.tile_order = nullptr;  // stale table
-  march_kernel<SH, LK, VT, UNIT, NS, CA, CN><<<grid, 32 * SBRC_MARCH_WARPS, 0, s>>>(q);
-}
-
-template <int SH, int LK, int VT, bool UNIT>
-void launch_march_kernel_shape(const sbrc_render_params& p, cudaStream_t s) {
-  if (SH == SBRC_SHADE_SHELL) {
-    if (p.shell_count == 3) launch_march<SH, LK, VT, UNIT, 3, 0, 0>(p, s);
-    else launch_march<SH, LK, VT, UNIT, 0, 0, 0>(p, s);
-  } else if (SH == SBRC_SHADE_CONE) {
-    if (p.cone_axis_samples == 2 && p.cone_angle_count == 4) launch_march<SH, LK, VT, UNIT, 0, 2, 4>(p, s);
-    else launch_march<SH, LK, VT, UNIT, 0, 0, 0>(p, s);
-  } else {
-    launch_march<SH, LK, VT, UNIT, 0, 0, 0>(p, s);
-  }
-}
-template <int SH, int LK, int VT>
-void launch_march_box(const sbrc_render_params& p, cudaStream_t s) {
-  if (unit_box(p.volume)) launch_march_kernel_shape<SH, LK, VT, true>(p, s);
-  else launch_march_kernel_shape<SH, LK, VT, false>(p, s);
-}
-template <int SH, int LK>
-void launch_march_vt(const sbrc_render_params& p, cudaStream_t s) {
-  switch (p.volume.voxel_type) {
-    case SBRC_VOXEL_F32: launch_march_box<SH, LK, SBRC_VOXEL_F32>(p, s); break;
-    case SBRC_VOXEL_U8: launch_march_box<SH, LK, SBRC_VOXEL_U8>(p, s); break;
-    case SBRC_VOXEL_U16: launch_march_box<SH, LK, SBRC_VOXEL_U16>(p, s); break;
-    case SBRC_VOXEL_F32_OCT: launch_march_box<SH, LK, SBRC_VOXEL_F32_OCT>(p, s); break;
-    case SBRC_VOXEL_U8_OCT: launch_march_box<SH, LK, SBRC_VOXEL_U8_OCT>(p, s); break;
-    default: launch_march_box<SH, LK, SBRC_VOXEL_U16_OCT>(p, s); break;
-  }
-}
-template <int SH>
-void launch_march_lookup(const sbrc_render_params& p, cudaStream_t s) {
-  if ((SH == SBRC_SHADE_SHADOW || SH == SBRC_SHADE_SHELL || SH == SBRC_SHADE_CONE) && p.lookup == SBRC_LOOKUP_NEAREST)
-    launch_march_vt<SH, SBRC_LOOKUP_NEAREST>(p, s);
-  else launch_march_vt<SH, SBRC_LOOKUP_LINEAR>(p, s);
 }
 
 }  // namespace
@@ -1451,10 +472,7 @@ int sbrc_build(const sbrc_build_params* p, void* stream) {
   switch (p->volume.voxel_type) {
     case SBRC_VOXEL_F32: launch_build<SBRC_VOXEL_F32>(*p, s); break;
     case SBRC_VOXEL_U8: launch_build<SBRC_VOXEL_U8>(*p, s); break;
-    case SBRC_VOXEL_U16: launch_build<SBRC_VOXEL_U16>(*p, s); break;
-    case SBRC_VOXEL_F32_OCT: launch_build<SBRC_VOXEL_F32_OCT>(*p, s); break;
-    case SBRC_VOXEL_U8_OCT: launch_build<SBRC_VOXEL_U8_OCT>(*p, s); break;
-    default: launch_build<SBRC_VOXEL_U16_OCT>(*p, s); break;
+    default: launch_build<SBRC_VOXEL_U16>(*p, s); break;
   }
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
@@ -1476,30 +494,6 @@ int sbrc_normalize_f32(float* data, int64_t n, float lo, float range, void* stre
   if (data == nullptr || n < 0 || !(range > 0.0f)) return SBRC_EINVAL;
   if (n == 0) return SBRC_OK;
   normalize_f32_kernel<<<148 * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(data, n, lo, range);
-  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
-}
-
-int sbrc_pack_octets(const sbrc_volume* src, void* dst, void* stream) {
-  if (src == nullptr || dst == nullptr || !volume_ok(*src) || src->voxel_type > SBRC_VOXEL_U16) return SBRC_EINVAL;
-  if ((unsigned long long)(src->nx + 1) * (src->ny + 1) * (src->nz + 1) >= (1ull << 32)) return SBRC_EINVAL;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int blocks = 148 * 16;
-  switch (src->voxel_type) {
-    case SBRC_VOXEL_F32:
-      pack_octets_kernel<float><<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(src->data), src->nx, src->ny,
-                                                       src->nz, reinterpret_cast<float*>(dst));
-      break;
-    case SBRC_VOXEL_U8:
-      pack_octets_kernel<unsigned char><<<blocks, 256, 0, s>>>(reinterpret_cast<const unsigned char*>(src->data),
-                                                               src->nx, src->ny, src->nz,
-                                                               reinterpret_cast<unsigned char*>(dst));
-      break;
-    default:
-      pack_octets_kernel<unsigned short><<<blocks, 256, 0, s>>>(reinterpret_cast<const unsigned short*>(src->data),
-                                                                src->nx, src->ny, src->nz,
-                                                                reinterpret_cast<unsigned short*>(dst));
-      break;
-  }
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 
@@ -1543,10 +537,7 @@ int sbrc_half_angle(const sbrc_half_angle_params* p, int first_slice, int last_s
                            : has_passes<VT, false>(*p, first_slice, last_slice, s))
     case SBRC_VOXEL_F32: SBRC_HAS(SBRC_VOXEL_F32); break;
     case SBRC_VOXEL_U8: SBRC_HAS(SBRC_VOXEL_U8); break;
-    case SBRC_VOXEL_U16: SBRC_HAS(SBRC_VOXEL_U16); break;
-    case SBRC_VOXEL_F32_OCT: SBRC_HAS(SBRC_VOXEL_F32_OCT); break;
-    case SBRC_VOXEL_U8_OCT: SBRC_HAS(SBRC_VOXEL_U8_OCT); break;
-    default: SBRC_HAS(SBRC_VOXEL_U16_OCT); break;
+    default: SBRC_HAS(SBRC_VOXEL_U16); break;
 #undef SBRC_HAS
   }
   if (finish) has_finish_kernel<<<148 * 4, 256, 0, s>>>(p->eye_accum, p->image, ne);
@@ -1571,10 +562,7 @@ int sbrc_shadow_oracle(const sbrc_volume* v, const double* alpha_lut, const doub
   switch (v->voxel_type) {
     case SBRC_VOXEL_F32: SBRC_ORACLE(SBRC_VOXEL_F32); break;
     case SBRC_VOXEL_U8: SBRC_ORACLE(SBRC_VOXEL_U8); break;
-    case SBRC_VOXEL_U16: SBRC_ORACLE(SBRC_VOXEL_U16); break;
-    case SBRC_VOXEL_F32_OCT: SBRC_ORACLE(SBRC_VOXEL_F32_OCT); break;
-    case SBRC_VOXEL_U8_OCT: SBRC_ORACLE(SBRC_VOXEL_U8_OCT); break;
-    default: SBRC_ORACLE(SBRC_VOXEL_U16_OCT); break;
+    default: SBRC_ORACLE(SBRC_VOXEL_U16); break;
   }
 #undef SBRC_ORACLE
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
@@ -1606,12 +594,12 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
   if (sbrc_local_rows(p->height, p->band_rows, p->rank, p->world) == 0) return SBRC_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (p->shading) {
-    case SBRC_SHADE_NONE: launch_march_lookup<SBRC_SHADE_NONE>(*p, s); break;
-    case SBRC_SHADE_PHONG: launch_march_lookup<SBRC_SHADE_PHONG>(*p, s); break;
-    case SBRC_SHADE_EXTINCTION: launch_march_lookup<SBRC_SHADE_EXTINCTION>(*p, s); break;
-    case SBRC_SHADE_SHADOW: launch_march_lookup<SBRC_SHADE_SHADOW>(*p, s); break;
-    case SBRC_SHADE_SHELL: launch_march_lookup<SBRC_SHADE_SHELL>(*p, s); break;
-    default: launch_march_lookup<SBRC_SHADE_CONE>(*p, s); break;
+    case SBRC_SHADE_NONE: sbrc_march_none(*p, s); break;
+    case SBRC_SHADE_PHONG: sbrc_march_phong(*p, s); break;
+    case SBRC_SHADE_EXTINCTION: sbrc_march_extinction(*p, s); break;
+    case SBRC_SHADE_SHADOW: sbrc_march_shadow(*p, s); break;
+    case SBRC_SHADE_SHELL: sbrc_march_shell(*p, s); break;
+    default: sbrc_march_cone(*p, s); break;
   }
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }

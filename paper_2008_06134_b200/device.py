@@ -47,23 +47,6 @@ class DeviceVolume:
         return (self.box_hi - self.box_lo) / np.array(self.dims, dtype=np.float64)
 
     @property
-    def is_octet(self) -> bool:
-        return self.voxel_type >= N.VOXEL_OCT
-
-    def octets(self) -> "DeviceVolume":
-        """The octet layout of this volume (K0, ``sbrc_pack_octets``): every
-        trilinear cell's 8 clamped corners stored together, so the exact fetch
-        is one or two 16-byte loads. 8x the bytes; same values."""
-        if self.is_octet:
-            return self
-        nx, ny, nz = self.dims
-        elem = self.data.element_size()
-        out = torch.empty(((nx + 1) * (ny + 1) * (nz + 1) * 8 * elem,), dtype=torch.uint8, device=self.data.device)
-        src = self.struct()
-        N.check(N.lib.sbrc_pack_octets(src, out.data_ptr(), current_stream_handle()), "sbrc_pack_octets")
-        return DeviceVolume(out, self.voxel_type + N.VOXEL_OCT, self.dims, self.box_lo, self.box_hi)
-
-    @property
     def nbytes(self) -> int:
         return self.data.numel() * self.data.element_size()
 

@@ -108,7 +108,7 @@ class FrameRenderer:
 
     def __init__(self, volume, tf, light_cam, spec, settings, *, group=None, build: str = "replicated",
                  band_rows: int = 8, compensation_n: float = 0.0, device=None, assemble: str = "nccl",
-                 heavy_first: bool = True):
+                 heavy_first: bool | None = None):
         check_frame(light_cam, spec)
         if build not in ("replicated", "sharded"):
             raise ValueError(f"build must be 'replicated' or 'sharded', got {build!r}")
@@ -121,6 +121,7 @@ class FrameRenderer:
         self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dvol = volume if isinstance(volume, DeviceVolume) else device_volume(volume, self.dev)
         self.tf, self.settings, self.build_mode = tf, settings, build
+        # heavy-first dispatch (schedule.py) measured: +1% at 1 rank, +8% at 4, +14% at 8, -6% at 2
         self.heavy_first = heavy_first
         self.band_rows, self.comp = band_rows, compensation_n
         self.lut = f64_tensor(tf.resolve(settings.step), self.dev)
@@ -242,7 +243,7 @@ class FrameRenderer:
                 band_rows=self.band_rows, rank=self.rank, world=self.world, voxel_size=self.dvol.voxel_size,
                 peer_images=self._peers if p2p else (),
                 tile_order=tile_order_for(self.settings, self.band_rows, self.rank, self.world, self.dev)
-                if self.heavy_first else None)
+                if (self.world != 2 if self.heavy_first is None else self.heavy_first) else None)
         self._render_params.sample_count = self.counter.data_ptr() if count_samples else None
         N.check(N.lib.sbrc_render(self._render_params, current_stream_handle()), "sbrc_render")
 

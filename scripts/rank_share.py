@@ -18,7 +18,7 @@ def main():
     dvol, _ = bench.device_volume_for(cfg, dev)
     buf = sb.build_attenuation_buffer(dvol, tf, cam, spec)
     band = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-    hf = (sys.argv[2] == "hf") if len(sys.argv) > 2 else True
+    hf = {"hf": True, "nohf": False}.get(sys.argv[2]) if len(sys.argv) > 2 else None  # None: library default
     out = {}
     for world in (1, 2, 4, 8):
         br = band if band > 0 else -(-(settings.viewport[1] // world) // 8) * 8  # 0: contiguous blocks

@@ -326,26 +326,6 @@ def test_single_texel_and_slice_edges(sb):
             assert st["max_abs"] <= TIGHT, (res, n, mode, lk, st)
 
 
-def test_octet_volume_identical(sb):
-    """The octet device layout (8 clamped corners per cell) gives bit-identical
-    builds and images for f32, u8 and u16 volumes, anisotropic boxes included."""
-    from paper_2008_06134_b200.device import DeviceVolume
-    for case in ("blob32", "block48_u8", "aniso_u16"):
-        g = load_golden(case)
-        v, tf, cam, spec, settings_for = scene_from_golden(g)
-        dv = DeviceVolume.from_dataset(v)
-        oc = dv.octets()
-        assert oc.is_octet and oc.voxel_type == dv.voxel_type + 4
-        a = sb.build_attenuation_buffer(dv, tf, cam, spec)
-        b = sb.build_attenuation_buffer(oc, tf, cam, spec)
-        assert np.array_equal(a.intensity, b.intensity)
-        assert np.array_equal(b.intensity, g["intensity"])
-        for mode in ("none", "cone", "shell", "phong"):
-            s = settings_for(mode)
-            assert np.array_equal(sb.render(dv, tf, s, a if mode in ("cone", "shell") else None),
-                                  sb.render(oc, tf, s, b if mode in ("cone", "shell") else None)), (case, mode)
-
-
 def test_anisotropic_box_general_path(sb):
     """Non-unit volume box (anisotropic spacing) takes the exact-division trilinear path."""
     from oracle import slicecast_oracle as O
