@@ -43,6 +43,9 @@
 #include <type_traits>
 
 // Compile-time variants (A/B'd in profiles/r01_notes.md).
+#ifndef SBRC_LATENCY_ALL
+#define SBRC_LATENCY_ALL 1  // latency mode also for shell / sbrc_shadow (config 1: 0.576 -> 0.511 ms)
+#endif
 #ifndef SBRC_LATENCY_MODE_PIXELS
 #define SBRC_LATENCY_MODE_PIXELS 196608  // rank-local pixels at or below which K2 runs 1 block/SM
 #endif
@@ -898,7 +901,9 @@ void launch_march(const sbrc_render_params& p, cudaStream_t s) {
   if (q.tile_order != nullptr && q.n_tiles != (int)(grid.x * grid.y)) q.tile_order = nullptr;  // stale table
   // latency mode for the default cone kernel when the rank-local image is small
   // (A/B in profiles/r01_notes.md: 131K px/rank 1.05 -> 0.75 ms; 262K px: 1.16 vs 1.28)
-  if constexpr (SH == SBRC_SHADE_CONE && CN > 0 && LK == SBRC_LOOKUP_LINEAR) {
+  if constexpr (LK == SBRC_LOOKUP_LINEAR &&
+                ((SH == SBRC_SHADE_CONE && CN > 0) || (SBRC_LATENCY_ALL && ((SH == SBRC_SHADE_SHELL && NS > 0) ||
+                                                                            SH == SBRC_SHADE_SHADOW)))) {
     if ((long long)p.width * q.local_rows <= SBRC_LATENCY_MODE_PIXELS) {
       march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1><<<grid, 32 * SBRC_MARCH_WARPS, 0, s>>>(q);
       return;
