@@ -147,10 +147,17 @@ class FrameRenderer:
     # -------------------------------------------------------------- p2p
     def _setup_p2p(self) -> None:
         h, w = self.height, self.width
-        self._raster = _DeviceBuffer(h * w * 16)
-        raster = torch.as_tensor(self._raster, device=self.dev).view(h, w, 4)
+        try:
+            self._raster = _DeviceBuffer(h * w * 16)
+            mine = self._raster.handle()
+        except RuntimeError:
+            self._raster, mine = None, b""
         handles = [None] * self.world
-        dist.all_gather_object(handles, self._raster.handle(), group=self.group)
+        dist.all_gather_object(handles, mine, group=self.group)
+        if not all(handles):  # every rank sees the same list: consistent fallback
+            self._fallback()
+            return
+        raster = torch.as_tensor(self._raster, device=self.dev).view(h, w, 4)
         peers, opened = [], []
         try:
             for r, hd in enumerate(handles):
@@ -165,60 +172,29 @@ class FrameRenderer:
             ok = False
         self._opened = opened
         self._barrier = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        # self-check: one frame both ways must agree bit for bit on every rank
-        if ok:
-            ref = self.frame().clone()
-            self._peers = peers
-            self._raster_t = raster
-            self.assemble_mode = "p2p"
-            self._render_params = None
-            got = self.frame()
-            ok = bool(torch.equal(ref, got))
-        flag = torch.tensor([0 if ok else 1], dtype=torch.int32,
-                            device=self.dev if dist.get_backend(self.group) == "nccl" else "cpu")
-        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
-        if int(flag.item()) != 0:
-            self._peers = []
-            self.assemble_mode = "nccl"
-            self._render_params = None
-
-    # -------------------------------------------------------------- light
-    def prepare_light(self, light_cam, spec):
-        """Device copies of a light frame's small inputs (alpha LUT at the slice
-        spacing, plane offsets), so a moving light costs no allocation per frame."""
-        check_frame(light_cam, spec)
-        return (light_cam, spec, f64_tensor(self.tf.resolve(spec.spacing)[:, 3], self.dev),
-                f64_tensor(spec.plane_offsets, self.dev))
-
-    def use_light(self, prepared) -> None:
-        """Switch to a prepared light frame; the buffer is reused when its shape is unchanged."""
-        cam, spec, alpha, offsets = prepared
-        shape = (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0]))
-        if getattr(self, "_shape", None) != shape:
-            self.set_light(cam, spec)
-        self.cam, self.spec, self.alpha, self.offsets = cam, spec, alpha, offsets
+        # both decisions are collective and taken in the same order on every
+        # rank, so a failure on one rank cannot desynchronise the collectives
+        if not self._all_ok(ok):  # some rank could not map a peer image
+            self._fallback()
+            return
+        ref = self.frame().clone()  # NCCL path
+        self._peers = peers
+        self._raster_t = raster
+        self.assemble_mode = "p2p"
         self._render_params = None
+        same = bool(torch.equal(ref, self.frame()))
+        if not self._all_ok(same):
+            self._fallback()
 
-    def set_light(self, light_cam, spec) -> None:
-        """(Re)allocate the attenuation buffer for a light frame (config 5 moves the light)."""
-        check_frame(light_cam, spec)
-        self.cam, self.spec = light_cam, spec
-        self.alpha = f64_tensor(self.tf.resolve(spec.spacing)[:, 3], self.dev)
-        self.offsets = f64_tensor(spec.plane_offsets, self.dev)
-        n, h, w = int(spec.n_slices), int(light_cam.resolution[1]), int(light_cam.resolution[0])
-        self._shape = (n, h, w)
-        if self.build_mode == "replicated" or self.world == 1:
-            self.storage = torch.empty((n, h, w, 4), dtype=torch.float32, device=self.dev)
-            self.quads = self.storage
-            self.shard = None
-        else:
-            b, e, hs = shard_rows(h, self.world, self.rank)
-            # row-major [H][n][W] quads: a rank's rows are one contiguous chunk
-            self.storage = torch.empty((self.world * hs, n, w, 4), dtype=torch.float32, device=self.dev)
-            self.shard_rows = (b, e)
-            self.shard = torch.empty((hs, n, w, 4), dtype=torch.float32, device=self.dev)
-            self.quads = self.storage[:h].permute(1, 0, 2, 3)  # (n, H, W, 4) view
-        self.intensity = self.quads[..., 0]
+    def _all_ok(self, ok: bool) -> bool:
+        nccl = dist.get_backend(self.group) == "nccl"
+        flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device=self.dev if nccl else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+        return int(flag.item()) == 0
+
+    def _fallback(self) -> None:
+        self._peers = []
+        self.assemble_mode = "nccl"
         self._render_params = None
 
     # -------------------------------------------------------------- stages
