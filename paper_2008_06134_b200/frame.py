@@ -197,6 +197,45 @@ class FrameRenderer:
         self.assemble_mode = "nccl"
         self._render_params = None
 
+    # -------------------------------------------------------------- light
+    def prepare_light(self, light_cam, spec):
+        """Device copies of a light frame's small inputs (alpha LUT at the slice
+        spacing, plane offsets), so a moving light costs no allocation per frame."""
+        check_frame(light_cam, spec)
+        return (light_cam, spec, f64_tensor(self.tf.resolve(spec.spacing)[:, 3], self.dev),
+                f64_tensor(spec.plane_offsets, self.dev))
+
+    def use_light(self, prepared) -> None:
+        """Switch to a prepared light frame; the buffer is reused when its shape is unchanged."""
+        cam, spec, alpha, offsets = prepared
+        shape = (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0]))
+        if getattr(self, "_shape", None) != shape:
+            self.set_light(cam, spec)
+        self.cam, self.spec, self.alpha, self.offsets = cam, spec, alpha, offsets
+        self._render_params = None
+
+    def set_light(self, light_cam, spec) -> None:
+        """(Re)allocate the attenuation buffer for a light frame (config 5 moves the light)."""
+        check_frame(light_cam, spec)
+        self.cam, self.spec = light_cam, spec
+        self.alpha = f64_tensor(self.tf.resolve(spec.spacing)[:, 3], self.dev)
+        self.offsets = f64_tensor(spec.plane_offsets, self.dev)
+        n, h, w = int(spec.n_slices), int(light_cam.resolution[1]), int(light_cam.resolution[0])
+        self._shape = (n, h, w)
+        if self.build_mode == "replicated" or self.world == 1:
+            self.storage = torch.empty((n, h, w, 4), dtype=torch.float32, device=self.dev)
+            self.quads = self.storage
+            self.shard = None
+        else:
+            b, e, hs = shard_rows(h, self.world, self.rank)
+            # row-major [H][n][W] quads: a rank's rows are one contiguous chunk
+            self.storage = torch.empty((self.world * hs, n, w, 4), dtype=torch.float32, device=self.dev)
+            self.shard_rows = (b, e)
+            self.shard = torch.empty((hs, n, w, 4), dtype=torch.float32, device=self.dev)
+            self.quads = self.storage[:h].permute(1, 0, 2, 3)  # (n, H, W, 4) view
+        self.intensity = self.quads[..., 0]
+        self._render_params = None
+
     # -------------------------------------------------------------- stages
     def build(self) -> None:
         if self.shard is None:
