@@ -70,11 +70,12 @@ def parse():
     ap.add_argument("--assemble", choices=("p2p", "nccl"), default="p2p",
                     help="N>1 image assembly: fused peer-memory stores from the march kernel (self-checked, "
                          "falls back to NCCL) or NCCL all-gather")
+    ap.add_argument("--raw-voxels", action="store_true",
+                    help="u8/u16 volumes: keep the integers in HBM (default: normalised to float32 once)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="N>1: disable overlapping the next frame's build with this frame's march")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--extra", action="store_true", help="also print a per-kernel detail line to stderr")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     return a
@@ -126,7 +127,7 @@ def device_volume_for(cfg, dev):
     d = cfg["dims"]
     if cfg["volume"] == "block_u8":
         v = host_volume(cfg)
-        return DeviceVolume.from_dataset(v, dev), v
+        return DeviceVolume.from_dataset(v, dev, widen=False), v
     q = "u16" if cfg["volume"] == "blobs_u16" else None
     t = datasets.sphere_blobs_device((d, d, d), seed=cfg["seed"], device=dev, quantize_to=q)
     kind = 2 if q else 0
@@ -347,6 +348,8 @@ def run_ours(a, cfg, mode):
     tf, cam, spec, settings = scene_objects(cfg, mode)
     t0 = time.perf_counter()
     dvol, host_vol = device_volume_for(cfg, dev)
+    if not a.raw_voxels:
+        dvol = dvol.widened()
     torch.cuda.synchronize()
     vol_gen_s = time.perf_counter() - t0
     fr = FrameRenderer(dvol, tf, cam, spec, settings, build=a.build if world > 1 else "replicated",
@@ -435,7 +438,7 @@ def run_ours(a, cfg, mode):
         e2e = e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev)
 
     # ---- roofline of the dominant kernel
-    vbytes = {0: 4, 1: 1, 2: 2}[dvol.voxel_type]  # algorithmic V counts the stored bytes per voxel
+    vbytes = {0: 4, 1: 1, 2: 2}[dvol.source_type]  # algorithmic V counts the source bytes per voxel
     V, A, I = algorithmic_bytes(cfg, vbytes, world)
     k1_bytes = V + (A if (world == 1 or a.build == "replicated") else A // world)
     k2_bytes = (V + A + I // world) if mode != "none" else (V + I // world)

@@ -7,9 +7,11 @@ a tightly packed little-endian (nz, ny, nx) grid of u8, u16 or f32 next to
 
 ``load_raw_device`` reads the file in chunks through two pinned host buffers
 and copies each chunk to the device asynchronously while the next is read.
-u8/u16 stay raw in HBM (the kernels normalise at fetch, bit-identically);
-f32 is min-max normalised on the device with numpy's float32 arithmetic
-(``sbrc_normalize_f32``). Nothing of the volume is kept on the host.
+u8/u16 cross the bus compact and are normalised once to float32 in HBM
+(or kept raw with ``widen=False``; the kernels then normalise at fetch,
+bit-identically); f32 is min-max normalised on the device with numpy's
+float32 arithmetic (``sbrc_normalize_f32``). Nothing of the volume is kept
+on the host.
 """
 
 from __future__ import annotations
@@ -97,9 +99,10 @@ def save_raw(v: VolumeDataset, raw_path, scalar_type: str = "u8") -> Path:
 
 
 def load_raw_device(path, meta: VolumeDescriptor | None = None, device=None,
-                    chunk_bytes: int = 64 << 20) -> DeviceVolume:
+                    chunk_bytes: int = 64 << 20, widen: bool = True) -> DeviceVolume:
     """Stream a .raw file into HBM (see module docstring). ``meta`` defaults to
-    the sidecar ``<path>.json``."""
+    the sidecar ``<path>.json``; ``widen`` normalises u8/u16 to float32 once
+    in HBM (DeviceVolume.widened)."""
     path = Path(path)
     meta = meta or VolumeDescriptor.from_json(path.with_suffix(".json"))
     dtype, total = _checked(path, meta)
@@ -131,9 +134,11 @@ def load_raw_device(path, meta: VolumeDescriptor | None = None, device=None,
     box_lo = (1.0 - frac) / 2.0
     box_hi = box_lo + frac
     if meta.scalar_type == "u8":
-        return DeviceVolume(out, N.VOXEL_U8, meta.dims, box_lo, box_hi)
+        dv = DeviceVolume(out, N.VOXEL_U8, meta.dims, box_lo, box_hi)
+        return dv.widened() if widen else dv
     if meta.scalar_type == "u16":
-        return DeviceVolume(out.view(torch.int16), N.VOXEL_U16, meta.dims, box_lo, box_hi)
+        dv = DeviceVolume(out.view(torch.int16), N.VOXEL_U16, meta.dims, box_lo, box_hi)
+        return dv.widened() if widen else dv
     data = out.view(torch.float32)
     lo, hi = (float(x) for x in torch.aminmax(data))
     if hi > lo:

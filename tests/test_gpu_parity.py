@@ -287,11 +287,12 @@ def test_u8_device_volume_is_raw(sb):
     from paper_2008_06134_b200.device import DeviceVolume
     g = load_golden("block48_u8")
     v, tf, cam, spec, settings_for = scene_from_golden(g)
-    dv = DeviceVolume.from_dataset(v)
+    dv = DeviceVolume.from_dataset(v, widen=False)
     assert dv.voxel_type == 1 and dv.nbytes == v.data.size
+    assert DeviceVolume.from_dataset(v).voxel_type == 0  # default: widened once in HBM
     g16 = load_golden("aniso_u16")
     v16 = scene_from_golden(g16)[0]
-    dv16 = DeviceVolume.from_dataset(v16)
+    dv16 = DeviceVolume.from_dataset(v16, widen=False)
     assert dv16.voxel_type == 2 and dv16.nbytes == 2 * v16.data.size
 
 
@@ -451,3 +452,20 @@ def test_geometry_edge_cases(sb, case):
             assert parity_stats(got, want)["max_abs"] <= TIGHT, (case, m)
         if case == "all_miss":
             assert np.all(got == 0.0)
+
+
+def test_widened_integer_volume_identical(sb):
+    """u8/u16 volumes normalised once to float32 in HBM render identically."""
+    from paper_2008_06134_b200.device import DeviceVolume
+    for case in ("block48_u8", "aniso_u16"):
+        g = load_golden(case)
+        v, tf, cam, spec, settings_for = scene_from_golden(g)
+        dv = DeviceVolume.from_dataset(v, widen=False)
+        wide = dv.widened()
+        assert wide.voxel_type == 0 and wide.source_type == dv.voxel_type
+        assert np.array_equal(wide.data.cpu().numpy().reshape(v.data.shape), v.data)
+        a = sb.build_attenuation_buffer(dv, tf, cam, spec)
+        b = sb.build_attenuation_buffer(wide, tf, cam, spec)
+        assert np.array_equal(a.intensity, b.intensity)
+        s = settings_for("cone")
+        assert np.array_equal(sb.render(dv, tf, s, a), sb.render(wide, tf, s, b))
