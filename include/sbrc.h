@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 2
+#define SBRC_ABI_VERSION 3
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -135,7 +135,11 @@ typedef struct sbrc_render_params {
   int32_t shell_count;
   int32_t cone_axis_samples;      /* ConeKernel.axis_samples              */
   int32_t cone_angle_count;
-  int32_t _pad;
+  /* Speed hint, results are identical either way: 1 = use the kernel that
+   * skips the light factor of samples whose (premultiplied) LUT emission is
+   * exactly zero — worth it when the volume holds values in the TF's leading
+   * zero-emission run (e.g. empty space at 0); 0 = evaluate every factor. */
+  int32_t skip_clear;
   double shell_radius[SBRC_MAX_SHELLS];
   double shell_weight[SBRC_MAX_SHELLS];
   double cone_ring;                /* ConeKernel.ring_radius_per_step     */

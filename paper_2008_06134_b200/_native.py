@@ -16,7 +16,7 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 MAX_PEERS = 8
@@ -63,7 +63,7 @@ class SbrcRenderParams(C.Structure):
                 ("quad_layer_stride", C.c_int64), ("quad_row_stride", C.c_int64),
                 ("light_color", C.c_float * 3), ("ambient_floor", C.c_float),
                 ("shell_count", C.c_int32), ("cone_axis_samples", C.c_int32),
-                ("cone_angle_count", C.c_int32), ("_pad", C.c_int32),
+                ("cone_angle_count", C.c_int32), ("skip_clear", C.c_int32),
                 ("shell_radius", C.c_double * MAX_SHELLS), ("shell_weight", C.c_double * MAX_SHELLS),
                 ("cone_ring", C.c_double), ("cone_cos", C.c_double * MAX_ANGLES),
                 ("cone_sin", C.c_double * MAX_ANGLES),

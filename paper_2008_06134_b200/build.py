@@ -16,8 +16,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-#: translation units: the C ABI + one per shading mode (K2 instantiations compile in parallel)
-SOURCES = ["sbrc.cu"] + [f"march_{m}.cu" for m in ("cone", "shell", "shadow", "none", "phong", "extinction")]
+#: translation units: the C ABI, and march_inst.cu once per (shading mode, voxel type) with the
+#: defines that select it (K2 instantiations compile in parallel; the cone ones are the long pole)
+UNITS = [("sbrc.cu", ())] + [("march_inst.cu", (f"SBRC_INST_SHADE={sh}", f"SBRC_INST_VT={vt}"))
+                             for sh in (5, 3, 2, 1, 4, 0) for vt in (0, 1, 2)]
+SOURCES = ["sbrc.cu", "march_inst.cu"]
 SRC = os.path.join(CSRC, "sbrc.cu")
 OUT = os.path.join(HERE, "_sbrc.so")
 
@@ -38,7 +41,7 @@ def nvcc() -> str:
 
 def build(verbose: bool = False, force: bool = False, out: str = OUT, defines=(), jobs: int | None = None) -> str:
     """Compile every translation unit (in parallel) and link ``out``; ``defines``
-    (e.g. ["SBRC_MARCH_MIN_BLOCKS=3"]) and ``out`` build experiment variants."""
+    (e.g. ["SBRC_WIDE_MAX_PIXELS=0"]) and ``out`` build experiment variants."""
     import concurrent.futures as cf
     import tempfile
     srcs = [os.path.join(CSRC, f) for f in SOURCES]
@@ -49,13 +52,16 @@ def build(verbose: bool = False, force: bool = False, out: str = OUT, defines=()
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     extra = [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else [])
 
-    def compile_one(src):
-        obj = os.path.join(tmp, os.path.basename(src) + ".o")
-        res = subprocess.run([nvcc(), *compile_flags, *extra, "-c", "-o", obj, src], capture_output=True, text=True)
+    def compile_one(unit):
+        name, defs = unit
+        src = os.path.join(CSRC, name)
+        obj = os.path.join(tmp, "_".join([name] + [d.split("=")[1] for d in defs]) + ".o")
+        res = subprocess.run([nvcc(), *compile_flags, *[f"-D{d}" for d in defs], *extra, "-c", "-o", obj, src],
+                             capture_output=True, text=True)
         return src, obj, res
 
-    with cf.ThreadPoolExecutor(max_workers=jobs or min(len(srcs), os.cpu_count() or 1)) as ex:
-        results = list(ex.map(compile_one, srcs))
+    with cf.ThreadPoolExecutor(max_workers=jobs or min(len(UNITS), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, UNITS))
     for src, obj, res in results:
         if verbose:
             sys.stderr.write(res.stderr)

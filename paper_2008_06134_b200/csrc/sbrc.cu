@@ -1,6 +1,6 @@
 // sbrc.cu — the C ABI of include/sbrc.h: K1 (attenuation build), the
 // point-wise light factor, shadow oracle, half-angle baseline, raw-volume
-// normalisation, IPC helpers, and K2 dispatch to march_<mode>.cu.
+// normalisation, IPC helpers, and K2 dispatch to march_inst.cu instances.
 // Kernel documentation and the numerics contract: sbrc_common.cuh.
 
 #include "sbrc_common.cuh"
@@ -446,10 +446,10 @@ int sbrc_ipc_close(void* ptr) { return cudaIpcCloseMemHandle(ptr) == cudaSuccess
 
 int sbrc_march_grid(int width, int height, int band_rows, int rank, int world, int* grid) {
   if (grid == nullptr) return SBRC_EINVAL;
-  constexpr int WX = SBRC_MARCH_WARPS_X, WY = SBRC_MARCH_WARPS / SBRC_MARCH_WARPS_X;
-  constexpr int BW = WX * SBRC_TILE_W, BH = WY * (32 / SBRC_TILE_W);
+  const int rows = sbrc_local_rows(height, band_rows, rank, world);
+  const int BW = (march_wide(width, rows) ? 4 : 2) * SBRC_TILE_W, BH = 2 * (32 / SBRC_TILE_W);
   grid[0] = (width + BW - 1) / BW;
-  grid[1] = (sbrc_local_rows(height, band_rows, rank, world) + BH - 1) / BH;
+  grid[1] = (rows + BH - 1) / BH;
   grid[2] = BW;
   grid[3] = BH;
   return SBRC_OK;
@@ -593,14 +593,12 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
     return SBRC_EINVAL;
   if (sbrc_local_rows(p->height, p->band_rows, p->rank, p->world) == 0) return SBRC_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  switch (p->shading) {
-    case SBRC_SHADE_NONE: sbrc_march_none(*p, s); break;
-    case SBRC_SHADE_PHONG: sbrc_march_phong(*p, s); break;
-    case SBRC_SHADE_EXTINCTION: sbrc_march_extinction(*p, s); break;
-    case SBRC_SHADE_SHADOW: sbrc_march_shadow(*p, s); break;
-    case SBRC_SHADE_SHELL: sbrc_march_shell(*p, s); break;
-    default: sbrc_march_cone(*p, s); break;
-  }
+  using march_fn = void (*)(const sbrc_render_params&, cudaStream_t);
+#define SBRC_MARCH_ROW(SH) {SBRC_MARCH_FN(SH, 0), SBRC_MARCH_FN(SH, 1), SBRC_MARCH_FN(SH, 2)}
+  static const march_fn kMarch[6][3] = {SBRC_MARCH_ROW(0), SBRC_MARCH_ROW(1), SBRC_MARCH_ROW(2),
+                                        SBRC_MARCH_ROW(3), SBRC_MARCH_ROW(4), SBRC_MARCH_ROW(5)};
+#undef SBRC_MARCH_ROW
+  kMarch[p->shading][p->volume.voxel_type](*p, s);
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 

@@ -1,8 +1,8 @@
 // sbrc_common.cuh — device code shared by the sbrc translation units: the
 // float64 reference arithmetic, voxel fetch and trilinear reconstruction,
 // light-space lookups, and the K2 march kernel template with its launch
-// dispatch. Each march_<mode>.cu instantiates one shading mode, so the
-// kernel variants compile in parallel.
+// dispatch. march_inst.cu instantiates one (shading mode, voxel type) per
+// compilation, so the kernel variants compile in parallel.
 #pragma once
 
 // sbrc.cu — B200 (sm_100a) kernels for slice-based ray casting with volume
@@ -49,12 +49,10 @@
 #ifndef SBRC_LATENCY_MODE_PIXELS
 #define SBRC_LATENCY_MODE_PIXELS 196608  // rank-local pixels at or below which K2 runs 1 block/SM
 #endif
-#ifndef SBRC_MARCH_WARPS
-#define SBRC_MARCH_WARPS 8  // warps per K2 block
+#ifndef SBRC_WIDE_MAX_PIXELS
+#define SBRC_WIDE_MAX_PIXELS 393216  // rank-local pixels at or below which K2 may use 8-warp blocks
 #endif
-#ifndef SBRC_MARCH_WARPS_X
-#define SBRC_MARCH_WARPS_X 4  // of which along x
-#endif
+#define SBRC_SM_COUNT 148  // B200
 #ifndef SBRC_CONE_PREFETCH
 #define SBRC_CONE_PREFETCH 0  // 1: cone tap quads loaded one sample ahead
 #endif
@@ -216,11 +214,13 @@ __device__ __forceinline__ void fill_u8_table(double* tab) {
 struct LutPos {
   int i0, i1;
   double f, g;
+  double t;  // LUT coordinate clip(s,0,1)*255
 };
 __device__ __forceinline__ LutPos lut_pos(double s) {
   LutPos r;
   const double t = dmul(dclip01(s), 255.0);
   const FloorD fl = floor_d(t);
+  r.t = t;
   r.i0 = fl.i;
   r.i1 = min(r.i0 + 1, SBRC_LUT_SIZE - 1);
   r.f = dsub(t, fl.f);
@@ -399,19 +399,35 @@ struct ShellTap {
 #ifndef SBRC_MARCH_PREFETCH
 #define SBRC_MARCH_PREFETCH 1
 #endif
-#ifndef SBRC_MARCH_MIN_BLOCKS
-#define SBRC_MARCH_MIN_BLOCKS 2  // 128 registers, no spills: 16 warps per SM (A/B in profiles/r01_notes.md)
+#ifndef SBRC_FACTOR_FIRST
+#define SBRC_FACTOR_FIRST 0  // light factor evaluated before the sample's scalar path
 #endif
+#ifndef SBRC_SKIP_CLEAR
+#define SBRC_SKIP_CLEAR 1  // instantiate the zero-emission skip (sbrc_render_params.skip_clear)
+#endif
+#if SBRC_SKIP_CLEAR && SBRC_CONE_PREFETCH
+#error "SBRC_CONE_PREFETCH pipelines the cone taps of every sample; build it with SBRC_SKIP_CLEAR=0"
+#endif
+// K2 block shape. NW = 4: 4-warp blocks of 16 x 8 pixels; NW = 8: 8-warp
+// blocks of 32 x 8 pixels. The 8-warp shape wins for mid-sized rank-local
+// images that still give >= 2 blocks per SM (a rank's share at 4-8 GPUs),
+// the 4-warp shape for full frames and tiny images (A/B in
+// profiles/r01_notes.md). Host and library use this one rule for the grid.
+inline bool march_wide(int width, int local_rows) {
+  const long long px = (long long)width * local_rows;
+  const long long blocks8 = (long long)((width + 31) / 32) * ((local_rows + 7) / 8);
+  return px <= SBRC_WIDE_MAX_PIXELS && blocks8 >= 2 * SBRC_SM_COUNT;
+}
 
-// MINB: resident blocks per SM the kernel is compiled for. The default
-// (SBRC_MARCH_MIN_BLOCKS = 2, 128 registers) maximises throughput when the
-// grid has many blocks per SM; MINB = 1 (up to 255 registers, more loads in
-// flight per warp) minimises per-warp latency, which decides the kernel time
-// when a rank's share of the image is small (its longest rays run nearly
-// alone at the end).
-template <int SHADING, int LOOKUP, int VT, bool UNIT, int NSHELL, int CONE_A, int CONE_N,
-          int MINB = SBRC_MARCH_MIN_BLOCKS>
-__global__ void __launch_bounds__(32 * SBRC_MARCH_WARPS, MINB) march_kernel(const sbrc_render_params P) {
+// MINB: resident blocks per SM the kernel is compiled for. The throughput
+// kernels (MINB = 16 warps per SM / NW: 128 registers) maximise throughput
+// when the grid has many blocks per SM; MINB = 1 (up to 255 registers, more
+// loads in flight per warp) minimises per-warp latency, which decides the
+// kernel time when a rank's share of the image is small (its longest rays run
+// nearly alone at the end). SKIP: see sbrc_render_params.skip_clear.
+template <int SHADING, int LOOKUP, int VT, bool UNIT, int NSHELL, int CONE_A, int CONE_N, int MINB, bool SKIP,
+          int NW>
+__global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_params P) {
   __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
@@ -464,12 +480,24 @@ __global__ void __launch_bounds__(32 * SBRC_MARCH_WARPS, MINB) march_kernel(cons
     for (int i = threadIdx.x; i < P.cone_angle_count; i += blockDim.x)
       cone_cs[i] = make_float2((float)P.cone_cos[i], (float)P.cone_sin[i]);
   }
+  __shared__ int lut_lit;  // first LUT entry with non-zero emission
+  if (threadIdx.x == 0) lut_lit = SBRC_LUT_SIZE;
   __syncthreads();
+  if constexpr (SKIP) {
+  // Leading run of LUT entries whose (premultiplied) emission is exactly 0:
+  // a sample with LUT coordinate t <= lut_lit - 1 interpolates two such
+  // entries (or one, with weight 1), so it adds nothing whatever the light
+  // factor, and the factor's lookups are skipped (bit-identical).
+  for (int i = threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x)
+    if (lut[2 * i].x != 0.0 || lut[2 * i].y != 0.0 || lut[2 * i + 1].x != 0.0) atomicMin(&lut_lit, i);
+  __syncthreads();
+  }
+  const double clear_t = (double)(lut_lit - 1);
 
   // Pixel of this lane: each warp owns a TILE_W x (32/TILE_W) pixel tile, a
-  // block 4 x 2 warp tiles.
+  // block WX x 2 warp tiles.
   constexpr int TW = SBRC_TILE_W, TH = 32 / SBRC_TILE_W;
-  constexpr int WX = SBRC_MARCH_WARPS_X, WY = SBRC_MARCH_WARPS / SBRC_MARCH_WARPS_X;
+  constexpr int WX = NW / 2, WY = 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int bx = blockIdx.x, by = blockIdx.y;
   if (P.tile_order != nullptr) {  // heavy-first dispatch: this block renders tile tile_order[b]
@@ -646,34 +674,9 @@ __global__ void __launch_bounds__(32 * SBRC_MARCH_WARPS, MINB) march_kernel(cons
       };
       bool cq_ok = CQ ? cone_issue(0.0f, t) : false;
 #endif
-      while (t < t_far && alpha < thresh) {
-#if SBRC_MARCH_PREFETCH
-        const double tn = dadd(t, step);
-        Cell<VT> nxt;
-        bool nxt_in;
-        {
-          const double qx = dadd(P.eye[0], dmul(tn, d[0]));
-          const double qy = dadd(P.eye[1], dmul(tn, d[1]));
-          const double qz = dadd(P.eye[2], dmul(tn, d[2]));
-          nxt_in = in_cube(qx, qy, qz);
-          if (nxt_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, nxt);
-        }
-        const double s = cur_in ? cell_combine<VT>(cur, reinterpret_cast<const float*>(u8tab)) : 0.0;
-#else
-        const double qx = dadd(P.eye[0], dmul(t, d[0]));
-        const double qy = dadd(P.eye[1], dmul(t, d[1]));
-        const double qz = dadd(P.eye[2], dmul(t, d[2]));
-        const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), qx, qy, qz);
-#endif
-        const LutPos q = lut_pos(s);
-        const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
-        const double2 b_rg = lut[2 * q.i1], b_ba = lut[2 * q.i1 + 1];
-        const double sr = dadd(dmul(a_rg.x, q.g), dmul(b_rg.x, q.f));
-        const double sg = dadd(dmul(a_rg.y, q.g), dmul(b_rg.y, q.f));
-        const double sb = dadd(dmul(a_ba.x, q.g), dmul(b_ba.x, q.f));
-        const double sa = dadd(dmul(a_ba.y, q.g), dmul(b_ba.y, q.f));
-
-        double fr = 1.0, fg = 1.0, fb = 1.0;
+      // Light factor of the sample at t (sample counter jf): independent of
+      // the sample's scalar, so it may be evaluated before or after it.
+      auto light_factor = [&](double& fr, double& fg, double& fb) {
         if (SHADING == SBRC_SHADE_PHONG || SHADING == SBRC_SHADE_EXTINCTION) {
           const double p[3] = {dadd(P.eye[0], dmul(t, d[0])), dadd(P.eye[1], dmul(t, d[1])),
                                dadd(P.eye[2], dmul(t, d[2]))};
@@ -828,6 +831,43 @@ __global__ void __launch_bounds__(32 * SBRC_MARCH_WARPS, MINB) march_kernel(cons
             fb = fb_c > 0.f ? (double)(fmaxf(scalar * fb_c, P.ambient_floor) * ib) : 1.0;
           }
         }
+      };
+      while (t < t_far && alpha < thresh) {
+#if SBRC_FACTOR_FIRST
+        double fr = 1.0, fg = 1.0, fb = 1.0;
+        light_factor(fr, fg, fb);
+#endif
+#if SBRC_MARCH_PREFETCH
+        const double tn = dadd(t, step);
+        Cell<VT> nxt;
+        bool nxt_in;
+        {
+          const double qx = dadd(P.eye[0], dmul(tn, d[0]));
+          const double qy = dadd(P.eye[1], dmul(tn, d[1]));
+          const double qz = dadd(P.eye[2], dmul(tn, d[2]));
+          nxt_in = in_cube(qx, qy, qz);
+          if (nxt_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, nxt);
+        }
+        const double s = cur_in ? cell_combine<VT>(cur, reinterpret_cast<const float*>(u8tab)) : 0.0;
+#else
+        const double qx = dadd(P.eye[0], dmul(t, d[0]));
+        const double qy = dadd(P.eye[1], dmul(t, d[1]));
+        const double qz = dadd(P.eye[2], dmul(t, d[2]));
+        const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), qx, qy, qz);
+#endif
+        const LutPos q = lut_pos(s);
+        const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
+        const double2 b_rg = lut[2 * q.i1], b_ba = lut[2 * q.i1 + 1];
+        const double sr = dadd(dmul(a_rg.x, q.g), dmul(b_rg.x, q.f));
+        const double sg = dadd(dmul(a_rg.y, q.g), dmul(b_rg.y, q.f));
+        const double sb = dadd(dmul(a_ba.x, q.g), dmul(b_ba.x, q.f));
+        const double sa = dadd(dmul(a_ba.y, q.g), dmul(b_ba.y, q.f));
+
+#if !SBRC_FACTOR_FIRST
+        double fr = 1.0, fg = 1.0, fb = 1.0;
+        // premultiplied emission (transfer.py:74) is 0 up to clear_t
+        if (!SKIP || !(q.t <= clear_t)) light_factor(fr, fg, fb);
+#endif
         // C += (1-a)*rgb*factor; a += (1-a)*a_src (raycaster.py:436-438)
         const double one_m = dsub(1.0, alpha);
         cr = dadd(cr, dmul(dmul(one_m, sr), fr));
@@ -891,12 +931,12 @@ inline bool unit_box(const sbrc_volume& v) {
   return true;
 }
 
-template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN>
-void launch_march(const sbrc_render_params& p, cudaStream_t s) {
-  constexpr int WX = SBRC_MARCH_WARPS_X, WY = SBRC_MARCH_WARPS / SBRC_MARCH_WARPS_X;
-  constexpr int BW = WX * SBRC_TILE_W, BH = WY * (32 / SBRC_TILE_W);
+template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN, bool SKIP>
+void launch_march_skip(const sbrc_render_params& p, cudaStream_t s) {
   sbrc_render_params q = p;
   q.local_rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
+  const bool wide = march_wide(p.width, q.local_rows);
+  const int BW = (wide ? 4 : 2) * SBRC_TILE_W, BH = 2 * (32 / SBRC_TILE_W);
   dim3 grid((p.width + BW - 1) / BW, (q.local_rows + BH - 1) / BH);
   if (q.tile_order != nullptr && q.n_tiles != (int)(grid.x * grid.y)) q.tile_order = nullptr;  // stale table
   // latency mode for the default cone kernel when the rank-local image is small
@@ -905,11 +945,26 @@ void launch_march(const sbrc_render_params& p, cudaStream_t s) {
                 ((SH == SBRC_SHADE_CONE && CN > 0) || (SBRC_LATENCY_ALL && ((SH == SBRC_SHADE_SHELL && NS > 0) ||
                                                                             SH == SBRC_SHADE_SHADOW)))) {
     if ((long long)p.width * q.local_rows <= SBRC_LATENCY_MODE_PIXELS) {
-      march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1><<<grid, 32 * SBRC_MARCH_WARPS, 0, s>>>(q);
+      if (wide) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 8><<<grid, 256, 0, s>>>(q);
+      else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4><<<grid, 128, 0, s>>>(q);
       return;
     }
   }
-  march_kernel<SH, LK, VT, UNIT, NS, CA, CN><<<grid, 32 * SBRC_MARCH_WARPS, 0, s>>>(q);
+  if (wide) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 2, SKIP, 8><<<grid, 256, 0, s>>>(q);
+  else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 4, SKIP, 4><<<grid, 128, 0, s>>>(q);
+}
+
+// skip_clear (a speed hint; results are identical either way) selects the
+// instantiation that skips the light factor of zero-emission samples.
+template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN>
+void launch_march(const sbrc_render_params& p, cudaStream_t s) {
+  if constexpr (SBRC_SKIP_CLEAR && SH != SBRC_SHADE_NONE) {
+    if (p.skip_clear) {
+      launch_march_skip<SH, LK, VT, UNIT, NS, CA, CN, true>(p, s);
+      return;
+    }
+  }
+  launch_march_skip<SH, LK, VT, UNIT, NS, CA, CN, false>(p, s);
 }
 
 template <int SH, int LK, int VT, bool UNIT>
@@ -929,30 +984,27 @@ void launch_march_box(const sbrc_render_params& p, cudaStream_t s) {
   if (unit_box(p.volume)) launch_march_kernel_shape<SH, LK, VT, true>(p, s);
   else launch_march_kernel_shape<SH, LK, VT, false>(p, s);
 }
-template <int SH, int LK>
-void launch_march_vt(const sbrc_render_params& p, cudaStream_t s) {
-  switch (p.volume.voxel_type) {
-    case SBRC_VOXEL_F32: launch_march_box<SH, LK, SBRC_VOXEL_F32>(p, s); break;
-    case SBRC_VOXEL_U8: launch_march_box<SH, LK, SBRC_VOXEL_U8>(p, s); break;
-    default: launch_march_box<SH, LK, SBRC_VOXEL_U16>(p, s); break;
-  }
-}
-template <int SH>
+template <int SH, int VT>
 void launch_march_lookup(const sbrc_render_params& p, cudaStream_t s) {
   if constexpr (SH == SBRC_SHADE_SHADOW || SH == SBRC_SHADE_SHELL || SH == SBRC_SHADE_CONE) {
     if (p.lookup == SBRC_LOOKUP_NEAREST) {
-      launch_march_vt<SH, SBRC_LOOKUP_NEAREST>(p, s);
+      launch_march_box<SH, SBRC_LOOKUP_NEAREST, VT>(p, s);
       return;
     }
   }
-  launch_march_vt<SH, SBRC_LOOKUP_LINEAR>(p, s);
+  launch_march_box<SH, SBRC_LOOKUP_LINEAR, VT>(p, s);
 }
 }  // namespace
 
-// One shading mode's K2 dispatch each (march_<mode>.cu).
-void sbrc_march_none(const sbrc_render_params& p, cudaStream_t s);
-void sbrc_march_shadow(const sbrc_render_params& p, cudaStream_t s);
-void sbrc_march_shell(const sbrc_render_params& p, cudaStream_t s);
-void sbrc_march_cone(const sbrc_render_params& p, cudaStream_t s);
-void sbrc_march_phong(const sbrc_render_params& p, cudaStream_t s);
-void sbrc_march_extinction(const sbrc_render_params& p, cudaStream_t s);
+// K2 dispatch for one (shading mode, voxel type): march_inst.cu compiled
+// once per pair (build.py), so the instantiations compile in parallel.
+#define SBRC_MARCH_FN_(SH, VT) sbrc_march_##SH##_##VT
+#define SBRC_MARCH_FN(SH, VT) SBRC_MARCH_FN_(SH, VT)
+#define SBRC_MARCH_DECL(SH, VT) void SBRC_MARCH_FN(SH, VT)(const sbrc_render_params& p, cudaStream_t s);
+#define SBRC_MARCH_DECL_VT(SH) SBRC_MARCH_DECL(SH, 0) SBRC_MARCH_DECL(SH, 1) SBRC_MARCH_DECL(SH, 2)
+SBRC_MARCH_DECL_VT(0)
+SBRC_MARCH_DECL_VT(1)
+SBRC_MARCH_DECL_VT(2)
+SBRC_MARCH_DECL_VT(3)
+SBRC_MARCH_DECL_VT(4)
+SBRC_MARCH_DECL_VT(5)

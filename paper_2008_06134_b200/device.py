@@ -1,12 +1,13 @@
 """Device residency: volume upload (K0), LUT upload and C-ABI parameter packing.
 
 Volume (K0). The reference keeps a float32 (nz, ny, nx) array normalised at
-load time (volume.py:141-151). On the device we keep the *raw* voxels when
-the dataset came from u8/u16 (1 or 2 bytes per voxel instead of 4): the
-kernels renormalise at fetch with an IEEE float32 division, which gives the
-same float32 value bit for bit. A volume is uploaded once and cached by
-array identity, the way the reference service keeps datasets resident
-(service.py:133-152); later calls with the same array only re-use it.
+load time (volume.py:141-151). A u8/u16 dataset crosses the bus in its raw
+encoding (1 or 2 bytes per voxel) and is normalised once in HBM to the same
+float32 values (``DeviceVolume.widened``, the default); kept raw, the kernels
+renormalise at fetch with an IEEE float32 division, bit for bit the same. A
+volume is uploaded once and cached by array identity, the way the reference
+service keeps datasets resident (service.py:133-152); later calls with the
+same array only re-use it.
 """
 
 from __future__ import annotations
@@ -41,6 +42,24 @@ class DeviceVolume:
         self.dims = tuple(int(d) for d in dims)
         self.box_lo = np.asarray(box_lo, dtype=np.float64)
         self.box_hi = np.asarray(box_hi, dtype=np.float64)
+        self._value_min = None
+
+    @property
+    def value_min(self) -> float:
+        """Smallest normalised voxel value (one reduction, cached; a speed hint
+        for the zero-emission skip, never a correctness input)."""
+        if self._value_min is None:
+            d = self.data.reshape(-1)
+            m = None
+            for b in range(0, d.numel(), 1 << 26):  # slabs bound the temporaries
+                c = d[b:b + (1 << 26)]
+                if self.voxel_type == N.VOXEL_U16:
+                    c = c.to(torch.int32) & 0xFFFF
+                cm = c.min()
+                m = cm if m is None else torch.minimum(m, cm)
+            scale = {N.VOXEL_F32: 1.0, N.VOXEL_U8: 255.0, N.VOXEL_U16: 65535.0}[self.voxel_type]
+            self._value_min = float(m) / scale
+        return self._value_min
 
     @property
     def voxel_size(self) -> np.ndarray:
@@ -60,7 +79,9 @@ class DeviceVolume:
         scale = 255.0 if self.voxel_type == N.VOXEL_U8 else 65535.0
         N.check(N.lib.sbrc_normalize_f32(f.data_ptr(), f.numel(), 0.0, scale, current_stream_handle()),
                 "sbrc_normalize_f32")
-        return DeviceVolume(f, N.VOXEL_F32, self.dims, self.box_lo, self.box_hi, source_type=self.voxel_type)
+        out = DeviceVolume(f, N.VOXEL_F32, self.dims, self.box_lo, self.box_hi, source_type=self.voxel_type)
+        out._value_min = self._value_min
+        return out
 
     @property
     def nbytes(self) -> int:
@@ -210,12 +231,29 @@ def pack_quads(plain: torch.Tensor, quads: torch.Tensor | None = None) -> torch.
     return quads
 
 
+def clear_entries(lut: np.ndarray) -> int:
+    """Length of the LUT's leading run of entries with zero (premultiplied)
+    emission: a sample whose LUT coordinate clip(s,0,1)*255 is at most
+    run - 1 adds exactly nothing to the pixel (raycaster.py:436)."""
+    nz = np.flatnonzero(np.any(np.asarray(lut)[:, :3] != 0.0, axis=1))
+    return int(nz[0]) if nz.size else len(lut)
+
+
+def skip_clear_hint(dvol: DeviceVolume, lut: np.ndarray) -> bool:
+    """Use the zero-emission skip when the volume reaches into that run
+    (some voxel's value maps there). Results are identical either way."""
+    run = clear_entries(lut)
+    return run >= 1 and dvol.value_min * 255.0 <= run - 1
+
+
 def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_cam, buffer_spec,
                   quads_dev: torch.Tensor | None, light_color, voxel_size_max: float,
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
-                  peer_images=(), tile_order: torch.Tensor | None = None) -> N.SbrcRenderParams:
-    """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469)."""
+                  peer_images=(), tile_order: torch.Tensor | None = None,
+                  lut_host: np.ndarray | None = None) -> N.SbrcRenderParams:
+    """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469).
+    ``lut_host`` (the resolved LUT on the host) enables the skip_clear hint."""
     mode = settings.shading_mode
     if mode not in N.SHADE:
         raise ValueError(f"unknown shading mode {mode!r}")
@@ -266,6 +304,8 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
         p.cone_ring = float(k.ring_radius_per_step)
         for i, th in enumerate(k.angles):
             p.cone_cos[i], p.cone_sin[i] = math.cos(th), math.sin(th)
+    if lut_host is not None and mode != "none":
+        p.skip_clear = int(skip_clear_hint(dvol, lut_host))
     p.band_rows, p.rank, p.world = int(band_rows), int(rank), int(world)
     p.image = image.data_ptr() if image is not None else None
     if len(peer_images) > N.MAX_PEERS:

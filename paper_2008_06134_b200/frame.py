@@ -124,7 +124,8 @@ class FrameRenderer:
         # heavy-first dispatch (schedule.py) measured: +1% at 1 rank, +8% at 4, +14% at 8, -6% at 2
         self.heavy_first = heavy_first
         self.band_rows, self.comp = band_rows, compensation_n
-        self.lut = f64_tensor(tf.resolve(settings.step), self.dev)
+        self.lut_host = tf.resolve(settings.step)
+        self.lut = f64_tensor(self.lut_host, self.dev)
         self.counter = torch.zeros(1, dtype=torch.int64, device=self.dev)
         w, h = int(settings.viewport[0]), int(settings.viewport[1])
         self.width, self.height = w, h
@@ -258,7 +259,8 @@ class FrameRenderer:
                 band_rows=self.band_rows, rank=self.rank, world=self.world, voxel_size=self.dvol.voxel_size,
                 peer_images=self._peers if p2p else (),
                 tile_order=tile_order_for(self.settings, self.band_rows, self.rank, self.world, self.dev)
-                if (self.world != 2 if self.heavy_first is None else self.heavy_first) else None)
+                if (self.world != 2 if self.heavy_first is None else self.heavy_first) else None,
+                lut_host=self.lut_host)
         self._render_params.sample_count = self.counter.data_ptr() if count_samples else None
         N.check(N.lib.sbrc_render(self._render_params, current_stream_handle()), "sbrc_render")
 

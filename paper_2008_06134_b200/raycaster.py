@@ -49,7 +49,8 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
         raise ValueError(f"unknown lookup mode {settings.lookup_mode!r}")
     dev = _require_cuda(device)
     dvol = device_volume(v, dev)
-    lut = f64_tensor(tf.resolve(settings.step), dev)   # raycaster.py:453
+    lut_host = tf.resolve(settings.step)   # raycaster.py:453
+    lut = f64_tensor(lut_host, dev)
     w, h = int(settings.viewport[0]), int(settings.viewport[1])
     if world == 1:
         band_rows = 8
@@ -71,7 +72,7 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
                       band_rows=band_rows, rank=rank, world=world, voxel_size=dvol.voxel_size,
                       peer_images=[int(x.data_ptr()) if isinstance(x, torch.Tensor) else int(x) for x in peer_images],
                       tile_order=tile_order_for(settings, band_rows, rank, world, dev)
-                      if (world != 2 if heavy_first is None else heavy_first) else None)
+                      if (world != 2 if heavy_first is None else heavy_first) else None, lut_host=lut_host)
     N.check(N.lib.sbrc_render(p, current_stream_handle()), "sbrc_render")
     img = out[:h] if world == 1 else out
     return (img, counter) if count_samples else img

@@ -469,3 +469,28 @@ def test_widened_integer_volume_identical(sb):
         assert np.array_equal(a.intensity, b.intensity)
         s = settings_for("cone")
         assert np.array_equal(sb.render(dv, tf, s, a), sb.render(wide, tf, s, b))
+
+
+@pytest.mark.parametrize("mode", ["sbrc_shadow", "shell", "cone", "phong", "extinction"])
+def test_zero_emission_skip_identical(sb, mode, monkeypatch):
+    """The skip_clear kernels (no light factor for zero-emission samples) give
+    the same bits as the kernels that evaluate every factor, on a volume with
+    empty space and a windowed TF whose first ~77 LUT entries emit nothing."""
+    from paper_2008_06134_b200 import device
+    from paper_2008_06134_b200.datasets import make_perforated_block
+    v = make_perforated_block((40, 40, 40), seed=5)
+    tf = sb.TransferFunction([(0.0, (0, 0, 0, 0)), (0.3, (0.2, 0.9, 0.1, 0.0)), (0.9, (1, 0.5, 0.2, 0.8)),
+                              (1.0, (1, 1, 1, 0.95))])
+    assert device.clear_entries(tf.resolve(1 / 128)) >= 76
+    d = (0.2, -0.4, 0.9)
+    settings = sb.RenderSettings(camera=sb.Camera(position=(1.4, 0.3, -1.2), target=(0.5, 0.5, 0.5)),
+                                 light=sb.Light(direction=d), viewport=(48, 40), step=1 / 128, shading_mode=mode)
+    buf = None
+    if mode in ("sbrc_shadow", "shell", "cone"):
+        buf = sb.build_attenuation_buffer(v, tf, sb.LightCamera.fit(d, (1, 1, 1), (40, 40)), sb.make_slice_stack(d, 32))
+    imgs = []
+    for hint in (True, False):
+        monkeypatch.setattr(device, "skip_clear_hint", lambda dvol, lut, h=hint: h)
+        imgs.append(sb.render(v, tf, settings, buf))
+    assert np.array_equal(imgs[0], imgs[1])
+    assert imgs[0][..., 3].max() > 0.1  # something was rendered

@@ -181,3 +181,25 @@ def test_multirank_assembly_gloo(world, h, br):
     for p in procs:
         p.join(timeout=60)
     assert all(ok_img and ok_buf for _, ok_img, ok_buf in res), res
+
+
+def test_skip_clear_hint():
+    """Leading zero-emission run of a LUT and the volume-minimum test that
+    selects the skip kernels (a speed hint only)."""
+    from paper_2008_06134_b200 import device
+    from paper_2008_06134_b200.scene import TransferFunction, preset
+    assert device.clear_entries(preset("hot").lut) == 1
+    assert device.clear_entries(np.zeros((256, 4))) == 256
+    lut = np.ones((256, 4))
+    assert device.clear_entries(lut) == 0
+    tf = TransferFunction([(0.0, (0, 0, 0, 0)), (0.5, (1, 1, 1, 0)), (1.0, (1, 1, 1, 1))])
+    run = device.clear_entries(tf.resolve(1 / 256))  # premultiplied (transfer.py:78-82)
+    assert 120 <= run <= 129
+
+    class V:
+        value_min = 0.0
+    assert device.skip_clear_hint(V, preset("hot").lut)
+    V.value_min = 0.001
+    assert not device.skip_clear_hint(V, preset("hot").lut)   # no voxel reaches the run
+    assert device.skip_clear_hint(V, tf.resolve(1 / 256))
+    assert not device.skip_clear_hint(V, lut)
