@@ -74,7 +74,7 @@ def parse():
                     help="u8/u16 volumes: keep the integers in HBM (default: normalised to float32 once)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true",
-                    help="N>1: disable overlapping the next frame's build with this frame's march")
+                    help="disable overlapping the next frame's build with this frame's march")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
@@ -366,7 +366,7 @@ def run_ours(a, cfg, mode):
         dist.all_reduce(t)
         samples = int(t.item())
 
-    pipelined = world > 1 and a.build == "replicated" and not a.no_pipeline
+    pipelined = (world == 1 or a.build == "replicated") and not a.no_pipeline
     pipe = FramePipeline(fr) if pipelined else None
 
     def one_step(ev=None):

@@ -23,7 +23,6 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   __syncthreads();
 
   const sbrc_light_frame& L = P.light;
-#if SBRC_BUILD_SHUFFLE
   // Warps are 32 consecutive texels of one row overlapping the next warp by
   // one: lane 31 only hands its layer pair to lane 30, so every quad is one
   // 16-byte store (the right neighbour's pair arrives by shuffle).
@@ -32,11 +31,6 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   const int y = P.row_begin + blockIdx.y * blockDim.y + threadIdx.y;
   if (y >= P.row_end) return;  // whole warp (warps are rows)
   const bool owner = lane < 31 && x < L.width;
-#else
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = P.row_begin + blockIdx.y * blockDim.y + threadIdx.y;
-  if (x >= L.width || y >= P.row_end) return;
-#endif
 
   // Texel centre in world (u, v) plane coordinates (_texel_world_grid, :134-141):
   // u0 + (i + 0.5) / W * (u1 - u0).
@@ -55,7 +49,6 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
   const float* tab = reinterpret_cast<const float*>(u8tab);
   double T = 1.0;
   float prev = 0.0f;
-#if SBRC_BUILD_SHUFFLE
   auto emit = [&](float4* layer_row, float a, float b) {
     float ra = __shfl_down_sync(0xffffffffu, a, 1), rb = __shfl_down_sync(0xffffffffu, b, 1);
     if (x == L.width - 1) {
@@ -64,9 +57,6 @@ __global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
     }
     if (owner) layer_row[x] = make_float4(a, b, ra, rb);
   };
-#else
-  auto emit = [&](float4* layer_row, float a, float b) { emit_pair(layer_row, x, L.width, a, b); };
-#endif
   // One slice of the recurrence: stored = T (:169); if covered, alpha from the
   // cell, optional compensation (:193-196), T *= 1 - alpha (:197-198).
   auto step_slice = [&](bool covered, const Cell<VT>& cl) -> float {
@@ -172,17 +162,7 @@ __global__ void __launch_bounds__(256) light_factor_kernel(const sbrc_render_par
   const double sx = (double)LF.width / (LF.u_range[1] - LF.u_range[0]);
   const double sy = (double)LF.height / (LF.v_range[1] - LF.v_range[0]);
   const double si = (double)LF.n_slices / (LF.d_max - LF.d_min);
-  QuadTex tex;
-  tex.q = reinterpret_cast<const float4*>(P.quads);
-  tex.qk = (unsigned)P.quad_layer_stride;
-  tex.qy = (unsigned)P.quad_row_stride;
-  tex.qy1 = LF.height > 1 ? tex.qy : 0u;
-  tex.txmax = (float)LF.width - 0.5f;
-  tex.tymax = (float)LF.height - 0.5f;
-  tex.xa_max = (float)max(LF.width - 2, 0);
-  tex.ya_max = (float)max(LF.height - 2, 0);
-  tex.li_max = (float)(LF.n_slices - 1);
-  tex.ka_max = (float)max(LF.n_slices - 2, 0);
+  const QuadTex tex = make_quad_tex(P);
   const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
   double pu = 0, pv = 0, pl = 0;
 #pragma unroll
@@ -379,12 +359,8 @@ void has_passes(const sbrc_half_angle_params& p, int k0, int k1, cudaStream_t s)
 
 template <int VT>
 void launch_build(const sbrc_build_params& p, cudaStream_t s) {
-  dim3 block(32, 8);
-#if SBRC_BUILD_SHUFFLE
+  dim3 block(32, 8);  // warps are rows of 31 owned texels (build_kernel)
   dim3 grid((p.light.width + 30) / 31, (p.row_end - p.row_begin + 7) / 8);
-#else
-  dim3 grid((p.light.width + 31) / 32, (p.row_end - p.row_begin + 7) / 8);
-#endif
   if (unit_box(p.volume)) build_kernel<VT, true><<<grid, block, 0, s>>>(p);
   else build_kernel<VT, false><<<grid, block, 0, s>>>(p);
 }

@@ -53,17 +53,14 @@
 #define SBRC_WIDE_MAX_PIXELS 393216  // rank-local pixels at or below which K2 may use 8-warp blocks
 #endif
 #define SBRC_SM_COUNT 148  // B200
-#ifndef SBRC_CONE_PREFETCH
-#define SBRC_CONE_PREFETCH 0  // 1: cone tap quads loaded one sample ahead
+#ifndef SBRC_NARROW_MINB
+#define SBRC_NARROW_MINB 4  // resident 4-warp blocks per SM of the throughput kernel (128 registers)
 #endif
 #ifndef SBRC_CONE_RING_SERIAL
 #define SBRC_CONE_RING_SERIAL 0  // 1: one cone ring's loads in flight at a time (fewer registers)
 #endif
 #ifndef SBRC_BUILD_UNROLL
 #define SBRC_BUILD_UNROLL 2  // slices whose gathers are in flight together in K1
-#endif
-#ifndef SBRC_BUILD_SHUFFLE
-#define SBRC_BUILD_SHUFFLE 1  // one 16-byte store per quad (warp shuffle for the x+1 neighbour)
 #endif
 
 namespace {
@@ -333,11 +330,33 @@ __device__ double phong_scalar(const sbrc_render_params& P, const float* u8tab, 
 // and the layer coordinate li = idx - 0.5 (lightbuffer.py:241-242, :279).
 struct QuadTex {
   const float4* q;
-  unsigned qk, qy, qy1;  // layer / row strides in quads; qy1 = row step to y+1 (0 if H == 1)
+  unsigned qk, qy;       // layer / row strides in quads
+  size_t qy64, qy1_64;   // row step as a 64-bit value; qy1_64: step to row y+1 (0 if H == 1)
   float txmax, tymax;    // footprint: u in [0,1]  <=>  tx in [-0.5, W-0.5]
   float xa_max, ya_max;  // max(W-2, 0), max(H-2, 0)
   float li_max, ka_max;  // n-1, max(n-2, 0)
 };
+
+// The row steps come from the 64-bit parameter, so the compiler cannot fold
+// (off + qy) into a 32-bit sum that needs zero-extending before the address
+// multiply (3 address instructions per two-row tap instead of 5; config 3
+// march 2.92 -> 2.85 ms).
+__device__ __forceinline__ QuadTex make_quad_tex(const sbrc_render_params& P) {
+  const sbrc_light_frame& LF = P.light;
+  QuadTex t;
+  t.q = reinterpret_cast<const float4*>(P.quads);
+  t.qk = (unsigned)P.quad_layer_stride;
+  t.qy = (unsigned)P.quad_row_stride;
+  t.qy64 = (size_t)P.quad_row_stride;
+  t.qy1_64 = LF.height > 1 ? t.qy64 : 0;
+  t.txmax = (float)LF.width - 0.5f;
+  t.tymax = (float)LF.height - 0.5f;
+  t.xa_max = (float)max(LF.width - 2, 0);
+  t.ya_max = (float)max(LF.height - 2, 0);
+  t.li_max = (float)(LF.n_slices - 1);
+  t.ka_max = (float)max(LF.n_slices - 2, 0);
+  return t;
+}
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b, fmaf(-t, a, a)); }
 
@@ -364,9 +383,9 @@ __device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float 
     ka = fminf(floor_f(li).f, t.ka_max);
     f = li - ka;
   }
-  const unsigned off = (unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa;
-  const float4 r0 = __ldg(t.q + off);
-  const float4 r1 = __ldg(t.q + off + t.qy1);
+  const float4* p = t.q + ((unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa);
+  const float4 r0 = __ldg(p);
+  const float4 r1 = __ldg(p + t.qy1_64);
   const float a0 = lerpf(r0.x, r0.z, fx), a1 = lerpf(r1.x, r1.z, fx);  // layer ka, rows y, y+1
   const float v0 = lerpf(a0, a1, fy);
   if (LOOKUP == SBRC_LOOKUP_NEAREST) return v0;
@@ -382,9 +401,9 @@ __device__ __forceinline__ void interior_tap(const QuadTex& t, unsigned kbase, f
                                              float& v1) {
   const FloorF xl = floor_f(tx), yl = floor_f(ty);
   const float fx = tx - xl.f, fy = ty - yl.f;
-  const unsigned off = kbase + (unsigned)yl.i * t.qy + (unsigned)xl.i;
-  const float4 r0 = __ldg(t.q + off);
-  const float4 r1 = __ldg(t.q + off + t.qy);
+  const float4* p = t.q + (kbase + (unsigned)yl.i * t.qy + (unsigned)xl.i);
+  const float4 r0 = __ldg(p);
+  const float4 r1 = __ldg(p + t.qy64);
   v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
   v1 += lerpf(lerpf(r0.y, r0.w, fx), lerpf(r1.y, r1.w, fx), fy);
 }
@@ -399,14 +418,8 @@ struct ShellTap {
 #ifndef SBRC_MARCH_PREFETCH
 #define SBRC_MARCH_PREFETCH 1
 #endif
-#ifndef SBRC_FACTOR_FIRST
-#define SBRC_FACTOR_FIRST 0  // light factor evaluated before the sample's scalar path
-#endif
 #ifndef SBRC_SKIP_CLEAR
 #define SBRC_SKIP_CLEAR 1  // instantiate the zero-emission skip (sbrc_render_params.skip_clear)
-#endif
-#if SBRC_SKIP_CLEAR && SBRC_CONE_PREFETCH
-#error "SBRC_CONE_PREFETCH pipelines the cone taps of every sample; build it with SBRC_SKIP_CLEAR=0"
 #endif
 // K2 block shape. NW = 4: 4-warp blocks of 16 x 8 pixels; NW = 8: 8-warp
 // blocks of 32 x 8 pixels. The 8-warp shape wins for mid-sized rank-local
@@ -553,16 +566,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       float fr_c = 1.f, fg_c = 1.f, fb_c = 1.f, ir = 1.f, ig = 1.f, ib = 1.f;
       constexpr bool BUFFERED = SHADING == SBRC_SHADE_SHADOW || SHADING == SBRC_SHADE_SHELL || SHADING == SBRC_SHADE_CONE;
       if (BUFFERED) {
-        tex.q = reinterpret_cast<const float4*>(P.quads);
-        tex.qk = (unsigned)P.quad_layer_stride;
-        tex.qy = (unsigned)P.quad_row_stride;
-        tex.qy1 = LF.height > 1 ? tex.qy : 0u;
-        tex.txmax = (float)LF.width - 0.5f;
-        tex.tymax = (float)LF.height - 0.5f;
-        tex.xa_max = (float)max(LF.width - 2, 0);
-        tex.ya_max = (float)max(LF.height - 2, 0);
-        tex.li_max = (float)(LF.n_slices - 1);
-        tex.ka_max = (float)max(LF.n_slices - 2, 0);
+        tex = make_quad_tex(P);
         double eu = 0, ev = 0, el = 0, du_ = 0, dv_ = 0, dl_ = 0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -639,43 +643,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         if (cur_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, cur);
       }
 #endif
-#if SBRC_CONE_PREFETCH
-      // Cone taps software-pipelined one sample ahead: the 16 quad loads of
-      // sample j+1 are issued right after sample j's taps are consumed and
-      // fly during sample j+1's alpha path (interior fast path only; the
-      // weights are recomputed from the same float inputs at consumption).
-      constexpr bool CQ = SHADING == SBRC_SHADE_CONE && CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR;
-      constexpr int NQ = CQ ? 2 * CONE_A * NA : 1;
-      float4 cq[NQ];
-      auto cone_issue = [&](float jv, double tv) -> bool {
-        if constexpr (!CQ) {
-          return false;
-        } else {
-          const float tx = fmaf(jv, ftxs, ftx0), ty = fmaf(jv, ftys, fty0), li = fmaf(jv, flis, fli0);
-          const bool fast = (double)dperp * tv > 1e-12 && tx - reach_x >= 0.f && tx + reach_x < fast_x_hi &&
-                            ty - reach_y >= 0.f && ty + reach_y < fast_y_hi && li - (float)CONE_A >= 0.f &&
-                            li - 1.0f < fast_l_hi;
-          if (!fast) return false;
-#pragma unroll
-          for (int i = 1; i <= CONE_A; ++i) {
-            const float r = spacing_r * (float)i;
-            const unsigned kb = (unsigned)floor_f(li - (float)i).i * tex.qk;
-#pragma unroll
-            for (int j = 0; j < NA; ++j) {
-              const FloorF xl = floor_f(fmaf(r, wx[j], tx)), yl = floor_f(fmaf(r, wy[j], ty));
-              const unsigned off = kb + (unsigned)yl.i * tex.qy + (unsigned)xl.i;
-              const int q = 2 * ((i - 1) * NA + j);
-              cq[q] = __ldg(tex.q + off);
-              cq[q + 1] = __ldg(tex.q + off + tex.qy);
-            }
-          }
-          return true;
-        }
-      };
-      bool cq_ok = CQ ? cone_issue(0.0f, t) : false;
-#endif
-      // Light factor of the sample at t (sample counter jf): independent of
-      // the sample's scalar, so it may be evaluated before or after it.
+      // Light factor of the sample at t (sample counter jf).
       auto light_factor = [&](double& fr, double& fg, double& fb) {
         if (SHADING == SBRC_SHADE_PHONG || SHADING == SBRC_SHADE_EXTINCTION) {
           const double p[3] = {dadd(P.eye[0], dmul(t, d[0])), dadd(P.eye[1], dmul(t, d[1])),
@@ -741,31 +709,6 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
           } else {  // cone
             const bool degenerate = !((double)dperp * t > 1e-12);  // fallback plane_basis(L)[0] = axis_u
             float acc = 0.0f;
-#if SBRC_CONE_PREFETCH
-            if constexpr (CQ) {
-              if (cq_ok) {
-#pragma unroll
-                for (int i = 1; i <= CONE_A; ++i) {
-                  const float r = spacing_r * (float)i;
-                  const float lt = li - (float)i;
-                  const FloorF kl = floor_f(lt);
-                  float v0 = 0.f, v1 = 0.f;
-#pragma unroll
-                  for (int j = 0; j < NA; ++j) {
-                    const float ttx = fmaf(r, wx[j], tx), tty = fmaf(r, wy[j], ty);
-                    const float fx = ttx - floor_f(ttx).f, fy = tty - floor_f(tty).f;
-                    const int q = 2 * ((i - 1) * NA + j);
-                    const float4 r0 = cq[q], r1 = cq[q + 1];
-                    v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
-                    v1 += lerpf(lerpf(r0.y, r0.w, fx), lerpf(r1.y, r1.w, fx), fy);
-                  }
-                  acc += lerpf(v0, v1, lt - kl.f);
-                }
-                scalar = acc * (1.0f / (float)(CONE_A * NA));
-              }
-            }
-            if (!(CQ && cq_ok)) {
-#endif
             const bool fast = CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR && !degenerate && tx - reach_x >= 0.f &&
                               tx + reach_x < fast_x_hi && ty - reach_y >= 0.f && ty + reach_y < fast_y_hi &&
                               li - (float)CONE_A >= 0.f && li - 1.0f < fast_l_hi;
@@ -818,10 +761,6 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
               }
               scalar = acc / (float)(P.cone_axis_samples * P.cone_angle_count);
             }
-#if SBRC_CONE_PREFETCH
-            }
-            if constexpr (CQ) cq_ok = cone_issue(jf + 1.0f, dadd(t, step));
-#endif
           }
           if (white) {
             fr = fg = fb = (double)fmaxf(scalar, 0.0f);
@@ -833,10 +772,6 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         }
       };
       while (t < t_far && alpha < thresh) {
-#if SBRC_FACTOR_FIRST
-        double fr = 1.0, fg = 1.0, fb = 1.0;
-        light_factor(fr, fg, fb);
-#endif
 #if SBRC_MARCH_PREFETCH
         const double tn = dadd(t, step);
         Cell<VT> nxt;
@@ -863,11 +798,9 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         const double sb = dadd(dmul(a_ba.x, q.g), dmul(b_ba.x, q.f));
         const double sa = dadd(dmul(a_ba.y, q.g), dmul(b_ba.y, q.f));
 
-#if !SBRC_FACTOR_FIRST
         double fr = 1.0, fg = 1.0, fb = 1.0;
         // premultiplied emission (transfer.py:74) is 0 up to clear_t
         if (!SKIP || !(q.t <= clear_t)) light_factor(fr, fg, fb);
-#endif
         // C += (1-a)*rgb*factor; a += (1-a)*a_src (raycaster.py:436-438)
         const double one_m = dsub(1.0, alpha);
         cr = dadd(cr, dmul(dmul(one_m, sr), fr));
@@ -951,7 +884,7 @@ void launch_march_skip(const sbrc_render_params& p, cudaStream_t s) {
     }
   }
   if (wide) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 2, SKIP, 8><<<grid, 256, 0, s>>>(q);
-  else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 4, SKIP, 4><<<grid, 128, 0, s>>>(q);
+  else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, SBRC_NARROW_MINB, SKIP, 4><<<grid, 128, 0, s>>>(q);
 }
 
 // skip_clear (a speed hint; results are identical either way) selects the
