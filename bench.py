@@ -145,24 +145,59 @@ def algorithmic_bytes(cfg, voxel_bytes, world):
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 50 ms; ``mark()``
-    brackets the timed region and only samples inside it are summarised."""
+    """SM clock, power and throttle reasons sampled during the timed region:
+    NVML polled every ~2 ms from a thread (so even a 50 ms region gets tens of
+    samples), nvidia-smi -lms 50 as the fallback. ``mark()`` brackets the
+    timed region and only samples inside it are summarised."""
 
     Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.thread = None
+        self.rows = []
         self.t0 = self.t1 = None
+        self.source = None
+
+    def _nvml_loop(self, nv, h, bits):
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((time.time(), float(sm), float(mx), pw,
+                                  [nm for nm, b in zip(self.NAMES, bits) if rs & b]))
+            except Exception:  # noqa: BLE001 - a failed poll is just a missing sample
+                pass
+            self.stop.wait(0.002)
 
     def __enter__(self):
+        try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(int(self.index))
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h, bits), daemon=True)
+            self.thread.start()
+            self.source = "nvml"
+            time.sleep(0.05)
+            return self
+        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
+            self.thread = None
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
+            self.source = "nvidia-smi"
         except OSError:
             self.proc = None
         time.sleep(0.4)
@@ -172,19 +207,19 @@ class ClockSampler:
         setattr(self, which, time.time())
 
     def __exit__(self, *exc):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=5)
         if self.proc is not None:
             time.sleep(0.1)
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
-    def summary(self):
+    def _smi_rows(self):
         import datetime as _dt
-        if self.proc is None:
-            return None
         self.f.flush()
         self.f.seek(0)
         rows = []
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for line in self.f.read().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
@@ -192,9 +227,18 @@ class ClockSampler:
             try:
                 ts = _dt.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
                 rows.append((ts, float(parts[1]), float(parts[2]), float(parts[3]),
-                             [nm for nm, val in zip(names, parts[4:8]) if val.lower() == "active"]))
+                             [nm for nm, val in zip(self.NAMES, parts[4:8]) if val.lower() == "active"]))
             except ValueError:
                 continue
+        return rows
+
+    def summary(self):
+        if self.thread is not None:
+            rows = list(self.rows)
+        elif self.proc is not None:
+            rows = self._smi_rows()
+        else:
+            return None
         if not rows:
             return None
         inside = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
@@ -204,7 +248,7 @@ class ClockSampler:
         reasons = sorted({nm for r in inside for nm in r[4]})
         return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": inside[0][2],
                 "power_w_max": max(r[3] for r in inside), "reasons": reasons, "samples": len(inside),
-                "window_s": (self.t1 - self.t0) if (self.t0 and self.t1) else None}
+                "window_s": (self.t1 - self.t0) if (self.t0 and self.t1) else None, "source": self.source}
 
 
 # --------------------------------------------------------------- CPU sample
