@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 3
+#define SBRC_ABI_VERSION 4
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -160,12 +160,19 @@ typedef struct sbrc_render_params {
    * process (CUDA IPC over NVLink). The caller then needs only a barrier. */
   float* peer_images[SBRC_MAX_PEERS];
   int32_t n_peers;
-  /* Optional dispatch order of the 2D block tiles (heavy-first scheduling):
-   * block b renders tile tile_order[b] (tile = ty * tiles_x + tx over the
-   * rank-local grid); NULL = natural order. n_tiles must equal the grid size. */
+  /* Optional dispatch order (heavy-first scheduling) over the rank-local
+   * tiles, tile = ty * tiles_x + tx: block tiles of sbrc_march_grid, or the
+   * 8x4-pixel warp tiles of sbrc_march_warp_grid when tile_counter is set;
+   * entry i is the tile dispatched i-th. NULL = natural order. n_tiles must
+   * equal the tile count (a stale table is ignored). */
   int32_t n_tiles;
   const int32_t* tile_order;
   unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
+  /* Persistent mode when non-NULL: the library zeroes this device word, then
+   * launches one resident grid whose warps pull 8x4-pixel warp tiles from it
+   * (atomic counter) until all are rendered — dynamic load balance at warp
+   * granularity instead of the block scheduler's. NULL = one block per tile. */
+  unsigned int* tile_counter;
 } sbrc_render_params;
 
 /* ABI version of the loaded library (== SBRC_ABI_VERSION). */
@@ -259,6 +266,9 @@ int sbrc_ipc_close(void* ptr);
 /* K2 grid for (width, height, band_rows, rank, world): grid[0..3] = tiles_x,
  * tiles_y, tile width and height in pixels (for building tile_order tables). */
 int sbrc_march_grid(int width, int height, int band_rows, int rank, int world, int grid[4]);
+
+/* The same for persistent mode (tile_counter set): warp tiles of 8 x 4 pixels. */
+int sbrc_march_warp_grid(int width, int height, int band_rows, int rank, int world, int grid[4]);
 
 /* Number of rank-local image rows sbrc_render writes for (height, band_rows, rank, world). */
 int sbrc_local_rows(int height, int band_rows, int rank, int world);

@@ -508,24 +508,42 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
   const double clear_t = (double)(lut_lit - 1);
 
   // Pixel of this lane: each warp owns a TILE_W x (32/TILE_W) pixel tile, a
-  // block WX x 2 warp tiles.
+  // block WX x 2 warp tiles. Persistent mode (tile_counter set): each warp
+  // pulls warp tiles from the counter until none are left, so a long tile
+  // holds one warp, not a whole block's slot.
   constexpr int TW = SBRC_TILE_W, TH = 32 / SBRC_TILE_W;
   constexpr int WX = NW / 2, WY = 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int bx = blockIdx.x, by = blockIdx.y;
-  if (P.tile_order != nullptr) {  // heavy-first dispatch: this block renders tile tile_order[b]
-    const int t = __ldg(P.tile_order + blockIdx.y * gridDim.x + blockIdx.x);
-    bx = t % gridDim.x;
-    by = t / gridDim.x;
+  const bool persistent = P.tile_counter != nullptr;
+  const int wtx = (P.width + TW - 1) / TW;
+  const int n_wt = wtx * ((P.local_rows + TH - 1) / TH);
+  unsigned int samples = 0;
+  for (int iter = 0;; ++iter) {
+  int px, lr;
+  if (persistent) {
+    int wt = 0;
+    if (lane == 0) wt = (int)atomicAdd(P.tile_counter, 1u);
+    wt = __shfl_sync(0xffffffffu, wt, 0);
+    if (wt >= n_wt) break;
+    if (P.tile_order != nullptr) wt = __ldg(P.tile_order + wt);
+    px = (wt % wtx) * TW + (lane % TW);
+    lr = (wt / wtx) * TH + (lane / TW);
+  } else {
+    if (iter > 0) break;
+    int bx = blockIdx.x, by = blockIdx.y;
+    if (P.tile_order != nullptr) {  // heavy-first dispatch: this block renders tile tile_order[b]
+      const int t = __ldg(P.tile_order + blockIdx.y * gridDim.x + blockIdx.x);
+      bx = t % gridDim.x;
+      by = t / gridDim.x;
+    }
+    px = bx * (WX * TW) + (warp % WX) * TW + (lane % TW);
+    lr = by * (WY * TH) + (warp / WX) * TH + (lane / TW);  // rank-local row
   }
-  const int px = bx * (WX * TW) + (warp % WX) * TW + (lane % TW);
-  const int lr = by * (WY * TH) + (warp / WX) * TH + (lane / TW);  // rank-local row
   const int band = lr / P.band_rows;
   const int py = (P.rank + band * P.world) * P.band_rows + (lr - band * P.band_rows);
   const bool in_image = px < P.width && lr < P.local_rows;
   const bool valid = in_image && py < P.height;
 
-  unsigned int samples = 0;
   float4 result = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
     // ---- Camera.rays (raycaster.py:53-68), numpy op order, float64.
@@ -828,6 +846,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       for (int i = 0; i < P.n_peers; ++i)
         reinterpret_cast<float4*>(P.peer_images[i])[(size_t)py * P.width + px] = result;
   }
+  }  // tile loop
   if (P.n_peers > 0) __threadfence_system();
   if (P.sample_count != nullptr) {
     const unsigned int tot = __reduce_add_sync(0xffffffffu, samples);
@@ -864,20 +883,44 @@ inline bool unit_box(const sbrc_volume& v) {
   return true;
 }
 
+// One resident grid (persistent mode): as many blocks as fit on the device
+// at once, capped by the work (warp tiles / warps per block).
+template <typename Kernel>
+void launch_resident(Kernel kernel, int threads, int n_wt, const sbrc_render_params& q, cudaStream_t s) {
+  int dev = 0, sms = SBRC_SM_COUNT, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  const int warps = threads / 32;
+  const int blocks = max(1, min(sms * max(per_sm, 1), (n_wt + warps - 1) / warps));
+  kernel<<<blocks, threads, 0, s>>>(q);
+}
+
 template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN, bool SKIP>
 void launch_march_skip(const sbrc_render_params& p, cudaStream_t s) {
   sbrc_render_params q = p;
   q.local_rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
+  // latency mode for the default cone kernel when the rank-local image is small
+  // (A/B in profiles/r01_notes.md: 131K px/rank 1.05 -> 0.75 ms; 262K px: 1.16 vs 1.28)
+  constexpr bool LAT = LK == SBRC_LOOKUP_LINEAR &&
+                       ((SH == SBRC_SHADE_CONE && CN > 0) ||
+                        (SBRC_LATENCY_ALL && ((SH == SBRC_SHADE_SHELL && NS > 0) || SH == SBRC_SHADE_SHADOW)));
+  const bool small = (long long)p.width * q.local_rows <= SBRC_LATENCY_MODE_PIXELS;
+  if (q.tile_counter != nullptr) {  // persistent mode: resident warps pull 8x4 warp tiles
+    const int n_wt = ((p.width + SBRC_TILE_W - 1) / SBRC_TILE_W) *
+                     ((q.local_rows + 32 / SBRC_TILE_W - 1) / (32 / SBRC_TILE_W));
+    if (q.tile_order != nullptr && q.n_tiles != n_wt) q.tile_order = nullptr;  // stale table
+    cudaMemsetAsync(q.tile_counter, 0, sizeof(unsigned int), s);
+    if (LAT && small) launch_resident(march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4>, 128, n_wt, q, s);
+    else launch_resident(march_kernel<SH, LK, VT, UNIT, NS, CA, CN, SBRC_NARROW_MINB, SKIP, 4>, 128, n_wt, q, s);
+    return;
+  }
   const bool wide = march_wide(p.width, q.local_rows);
   const int BW = (wide ? 4 : 2) * SBRC_TILE_W, BH = 2 * (32 / SBRC_TILE_W);
   dim3 grid((p.width + BW - 1) / BW, (q.local_rows + BH - 1) / BH);
   if (q.tile_order != nullptr && q.n_tiles != (int)(grid.x * grid.y)) q.tile_order = nullptr;  // stale table
-  // latency mode for the default cone kernel when the rank-local image is small
-  // (A/B in profiles/r01_notes.md: 131K px/rank 1.05 -> 0.75 ms; 262K px: 1.16 vs 1.28)
-  if constexpr (LK == SBRC_LOOKUP_LINEAR &&
-                ((SH == SBRC_SHADE_CONE && CN > 0) || (SBRC_LATENCY_ALL && ((SH == SBRC_SHADE_SHELL && NS > 0) ||
-                                                                            SH == SBRC_SHADE_SHADOW)))) {
-    if ((long long)p.width * q.local_rows <= SBRC_LATENCY_MODE_PIXELS) {
+  if constexpr (LAT) {
+    if (small) {
       if (wide) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 8><<<grid, 256, 0, s>>>(q);
       else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4><<<grid, 128, 0, s>>>(q);
       return;

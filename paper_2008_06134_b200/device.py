@@ -251,7 +251,8 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
                   peer_images=(), tile_order: torch.Tensor | None = None,
-                  lut_host: np.ndarray | None = None) -> N.SbrcRenderParams:
+                  lut_host: np.ndarray | None = None,
+                  tile_counter: torch.Tensor | None = None) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469).
     ``lut_host`` (the resolved LUT on the host) enables the skip_clear hint."""
     mode = settings.shading_mode
@@ -316,23 +317,27 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     if tile_order is not None:
         p.tile_order, p.n_tiles = tile_order.data_ptr(), int(tile_order.numel())
     p.sample_count = counter.data_ptr() if counter is not None else None
+    p.tile_counter = tile_counter.data_ptr() if tile_counter is not None else None
     return p
 
 
 _ORDER_CACHE: dict = {}
 
+#: K2 persistent mode (resident warps pulling 8x4 warp tiles; sbrc_render_params.tile_counter) by default
+PERSISTENT_DEFAULT = False
 
-def tile_order_for(settings, band_rows: int, rank: int, world: int, device) -> torch.Tensor:
+
+def tile_order_for(settings, band_rows: int, rank: int, world: int, device, warp_tiles: bool = False) -> torch.Tensor:
     """Device copy of the heavy-first dispatch table (schedule.heavy_first), cached per view."""
     from .schedule import heavy_first
     cam = settings.camera
     key = (tuple(np.asarray(cam.position, np.float64)), tuple(np.asarray(cam.target, np.float64)),
            tuple(np.asarray(cam.up, np.float64)), float(cam.fov_deg), tuple(settings.viewport), band_rows, rank,
-           world, str(device))
+           world, str(device), warp_tiles)
     t = _ORDER_CACHE.get(key)
     if t is None:
         if len(_ORDER_CACHE) > 64:
             _ORDER_CACHE.clear()
-        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world)).to(device)
+        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world, warp_tiles)).to(device)
         _ORDER_CACHE[key] = t
     return t

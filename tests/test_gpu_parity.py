@@ -494,3 +494,28 @@ def test_zero_emission_skip_identical(sb, mode, monkeypatch):
         imgs.append(sb.render(v, tf, settings, buf))
     assert np.array_equal(imgs[0], imgs[1])
     assert imgs[0][..., 3].max() > 0.1  # something was rendered
+
+
+@pytest.mark.parametrize("mode", ["none", "sbrc_shadow", "shell", "cone"])
+def test_persistent_march_identical(sb, mode):
+    """Persistent K2 (resident warps pulling 8x4 warp tiles from a counter,
+    natural or heavy-first order) renders the same bits and the same sample
+    count as one block per tile, for a full frame and a rank's share."""
+    import torch
+    from paper_2008_06134_b200.datasets import make_sphere_blobs
+    v = make_sphere_blobs((40, 40, 40), seed=7)
+    tf = sb.preset("hot")
+    d = (0.3, -0.5, 0.8)
+    settings = sb.RenderSettings(camera=sb.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5)),
+                                 light=sb.Light(direction=d), viewport=(100, 72), step=1 / 96, shading_mode=mode)
+    buf = None
+    if mode != "none":
+        buf = sb.build_attenuation_buffer(v, tf, sb.LightCamera.fit(d, (1, 1, 1), (48, 48)), sb.make_slice_stack(d, 24))
+    for rank, world in ((0, 1), (1, 3)):
+        ref, n_ref = sb.render_device(v, tf, settings, buf, rank=rank, world=world, count_samples=True,
+                                      persistent=False, heavy_first=False)
+        for hf in (False, True):
+            got, n = sb.render_device(v, tf, settings, buf, rank=rank, world=world, count_samples=True,
+                                      persistent=True, heavy_first=hf)
+            assert torch.equal(got, ref), (rank, world, hf)
+            assert int(n.item()) == int(n_ref.item())
