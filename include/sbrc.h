@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 4
+#define SBRC_ABI_VERSION 5
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -161,8 +161,7 @@ typedef struct sbrc_render_params {
   float* peer_images[SBRC_MAX_PEERS];
   int32_t n_peers;
   /* Optional dispatch order (heavy-first scheduling) over the rank-local
-   * tiles, tile = ty * tiles_x + tx: block tiles of sbrc_march_grid, or the
-   * 8x4-pixel warp tiles of sbrc_march_warp_grid when tile_counter is set;
+   * tiles of sbrc_render_grid, tile = ty * tiles_x + tx;
    * entry i is the tile dispatched i-th. NULL = natural order. n_tiles must
    * equal the tile count (a stale table is ignored). */
   int32_t n_tiles;
@@ -263,9 +262,17 @@ int sbrc_ipc_handle(void* ptr, unsigned char handle[64]);
 int sbrc_ipc_open(const unsigned char handle[64], void** ptr);
 int sbrc_ipc_close(void* ptr);
 
-/* K2 grid for (width, height, band_rows, rank, world): grid[0..3] = tiles_x,
- * tiles_y, tile width and height in pixels (for building tile_order tables). */
+/* Block grid of the throughput K2 kernels for (width, height, band_rows,
+ * rank, world): grid[0..3] = tiles_x, tiles_y, tile width and height in
+ * pixels. Latency mode and ray groups change the grid: build tile_order
+ * tables from sbrc_render_grid. */
 int sbrc_march_grid(int width, int height, int band_rows, int rank, int world, int grid[4]);
+
+/* The tile grid sbrc_render will launch for *p (block shape, latency mode,
+ * ray groups and persistent mode all depend on the params): grid[0..3] =
+ * tiles_x, tiles_y, tile width and height in pixels. tile_order tables must
+ * index this grid. */
+int sbrc_render_grid(const sbrc_render_params* p, int grid[4]);
 
 /* The same for persistent mode (tile_counter set): warp tiles of 8 x 4 pixels. */
 int sbrc_march_warp_grid(int width, int height, int band_rows, int rank, int world, int grid[4]);

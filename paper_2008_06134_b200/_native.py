@@ -16,7 +16,7 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 MAX_PEERS = 8
@@ -31,7 +31,7 @@ EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume
            "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_shadow_oracle", "sbrc_light_factor",
            "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_ipc_alloc", "sbrc_ipc_free", "sbrc_ipc_handle",
            "sbrc_ipc_open", "sbrc_ipc_close", "sbrc_march_grid", "sbrc_local_rows",
-           "sbrc_march_warp_grid")
+           "sbrc_march_warp_grid", "sbrc_render_grid")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -103,6 +103,7 @@ def _load() -> C.CDLL:
     lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
     lib.sbrc_march_grid.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int * 4]
     lib.sbrc_march_warp_grid.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int * 4]
+    lib.sbrc_render_grid.argtypes = [C.POINTER(SbrcRenderParams), C.c_int * 4]
     lib.sbrc_light_factor.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
     lib.sbrc_ipc_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
@@ -144,6 +145,13 @@ def check(status: int, what: str) -> None:
 
 def local_rows(height: int, band_rows: int, rank: int, world: int) -> int:
     return int(lib.sbrc_local_rows(height, band_rows, rank, world))
+
+
+def render_grid(p) -> tuple[int, int, int, int]:
+    """(tiles_x, tiles_y, tile_w, tile_h) sbrc_render launches for params ``p``."""
+    g = (C.c_int * 4)()
+    check(lib.sbrc_render_grid(C.byref(p), g), "sbrc_render_grid")
+    return g[0], g[1], g[2], g[3]
 
 
 def march_grid(width: int, height: int, band_rows: int, rank: int, world: int,

@@ -431,6 +431,18 @@ int sbrc_march_grid(int width, int height, int band_rows, int rank, int world, i
   return SBRC_OK;
 }
 
+int sbrc_render_grid(const sbrc_render_params* p, int* grid) {
+  if (p == nullptr || grid == nullptr || p->width < 1 || p->height < 1 || p->band_rows < 1 || p->world < 1 ||
+      p->rank < 0 || p->rank >= p->world)
+    return SBRC_EINVAL;
+  const MarchShape m = march_shape(*p, sbrc_local_rows(p->height, p->band_rows, p->rank, p->world));
+  grid[0] = m.tiles_x;
+  grid[1] = m.tiles_y;
+  grid[2] = m.bw;
+  grid[3] = m.bh;
+  return SBRC_OK;
+}
+
 int sbrc_march_warp_grid(int width, int height, int band_rows, int rank, int world, int* grid) {
   if (grid == nullptr) return SBRC_EINVAL;
   const int rows = sbrc_local_rows(height, band_rows, rank, world);

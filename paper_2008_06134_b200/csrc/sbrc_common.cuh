@@ -53,6 +53,12 @@
 #define SBRC_WIDE_MAX_PIXELS 393216  // rank-local pixels at or below which K2 may use 8-warp blocks
 #endif
 #define SBRC_SM_COUNT 148  // B200
+#ifndef SBRC_LAT_GROUP
+#define SBRC_LAT_GROUP 4  // lanes per ray for tiny rank-local images (2, 4, 8)
+#endif
+#ifndef SBRC_GROUP_PIXELS
+#define SBRC_GROUP_PIXELS 49152  // rank-local pixels at or below which latency mode uses ray groups
+#endif
 #ifndef SBRC_NARROW_MINB
 #define SBRC_NARROW_MINB 4  // resident 4-warp blocks per SM of the throughput kernel (128 registers)
 #endif
@@ -432,6 +438,45 @@ inline bool march_wide(int width, int local_rows) {
   return px <= SBRC_WIDE_MAX_PIXELS && blocks8 >= 2 * SBRC_SM_COUNT;
 }
 
+// Latency mode (MINB = 1, up to 255 registers; for tiny images also ray
+// groups of SBRC_LAT_GROUP lanes) exists for the unrolled default kernels of
+// the buffer modes with linear lookups; it is used when the rank-local image
+// is small. This must mirror the instantiation choice in
+// launch_march_kernel_shape.
+inline bool march_latency_kernel(const sbrc_render_params& p) {
+  if (p.lookup != SBRC_LOOKUP_LINEAR) return false;
+  if (p.shading == SBRC_SHADE_CONE) return p.cone_axis_samples == 2 && p.cone_angle_count == 4;
+  if (!SBRC_LATENCY_ALL) return false;
+  return (p.shading == SBRC_SHADE_SHELL && p.shell_count == 3) || p.shading == SBRC_SHADE_SHADOW;
+}
+
+// The K2 launch shape for these params: the one rule the launch and
+// sbrc_render_grid (heavy-first tables on the host) share.
+struct MarchShape {
+  bool persistent, latency;
+  int nw, group, bw, bh, tiles_x, tiles_y;
+};
+inline MarchShape march_shape(const sbrc_render_params& p, int local_rows) {
+  MarchShape m{};
+  m.persistent = p.tile_counter != nullptr;
+  m.latency = march_latency_kernel(p) && (long long)p.width * local_rows <= SBRC_LATENCY_MODE_PIXELS;
+  if (m.persistent) {  // warp tiles
+    m.nw = 4;
+    m.group = 1;
+    m.bw = SBRC_TILE_W;
+    m.bh = 32 / SBRC_TILE_W;
+  } else {
+    m.nw = march_wide(p.width, local_rows) ? 8 : 4;
+    m.group = m.latency && (long long)p.width * local_rows <= SBRC_GROUP_PIXELS ? SBRC_LAT_GROUP : 1;
+    const int tw = m.group == 1 ? SBRC_TILE_W : 4, th = (32 / m.group) / tw;
+    m.bw = (m.nw / 2) * tw;
+    m.bh = 2 * th;
+  }
+  m.tiles_x = (p.width + m.bw - 1) / m.bw;
+  m.tiles_y = (local_rows + m.bh - 1) / m.bh;
+  return m;
+}
+
 // MINB: resident blocks per SM the kernel is compiled for. The throughput
 // kernels (MINB = 16 warps per SM / NW: 128 registers) maximise throughput
 // when the grid has many blocks per SM; MINB = 1 (up to 255 registers, more
@@ -439,8 +484,11 @@ inline bool march_wide(int width, int local_rows) {
 // kernel time when a rank's share of the image is small (its longest rays run
 // nearly alone at the end). SKIP: see sbrc_render_params.skip_clear.
 template <int SHADING, int LOOKUP, int VT, bool UNIT, int NSHELL, int CONE_A, int CONE_N, int MINB, bool SKIP,
-          int NW>
+          int NW, int G>
 __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_params P) {
+  static_assert(G == 1 || SHADING == SBRC_SHADE_SHADOW || SHADING == SBRC_SHADE_SHELL || SHADING == SBRC_SHADE_CONE,
+                "ray groups carry float32 light factors (buffer modes)");
+  static_assert(G == 1 || SBRC_MARCH_PREFETCH, "ray groups use the prefetched cell");
   __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
@@ -507,13 +555,16 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
   }
   const double clear_t = (double)(lut_lit - 1);
 
-  // Pixel of this lane: each warp owns a TILE_W x (32/TILE_W) pixel tile, a
-  // block WX x 2 warp tiles. Persistent mode (tile_counter set): each warp
-  // pulls warp tiles from the counter until none are left, so a long tile
-  // holds one warp, not a whole block's slot.
-  constexpr int TW = SBRC_TILE_W, TH = 32 / SBRC_TILE_W;
+  // Pixel of this lane: each warp owns a TW x TH pixel tile, a block WX x 2
+  // warp tiles. Ray groups (G > 1): G adjacent lanes share one ray and take
+  // its samples round-robin (lane gl: samples gl, gl+G, ...), so a long ray
+  // runs G samples per serial step; warps then own 32/G rays. Persistent
+  // mode (tile_counter set, G == 1): each warp pulls warp tiles from the
+  // counter until none are left.
+  constexpr int TW = G == 1 ? SBRC_TILE_W : 4, TH = (32 / G) / TW;
   constexpr int WX = NW / 2, WY = 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ray = lane / G, gl = lane % G;
   const bool persistent = P.tile_counter != nullptr;
   const int wtx = (P.width + TW - 1) / TW;
   const int n_wt = wtx * ((P.local_rows + TH - 1) / TH);
@@ -526,8 +577,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
     wt = __shfl_sync(0xffffffffu, wt, 0);
     if (wt >= n_wt) break;
     if (P.tile_order != nullptr) wt = __ldg(P.tile_order + wt);
-    px = (wt % wtx) * TW + (lane % TW);
-    lr = (wt / wtx) * TH + (lane / TW);
+    px = (wt % wtx) * TW + (ray % TW);
+    lr = (wt / wtx) * TH + (ray / TW);
   } else {
     if (iter > 0) break;
     int bx = blockIdx.x, by = blockIdx.y;
@@ -536,8 +587,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       bx = t % gridDim.x;
       by = t / gridDim.x;
     }
-    px = bx * (WX * TW) + (warp % WX) * TW + (lane % TW);
-    lr = by * (WY * TH) + (warp / WX) * TH + (lane / TW);  // rank-local row
+    px = bx * (WX * TW) + (warp % WX) * TW + (ray % TW);
+    lr = by * (WY * TH) + (warp / WX) * TH + (ray / TW);  // rank-local row
   }
   const int band = lr / P.band_rows;
   const int py = (P.rank + band * P.world) * P.band_rows + (lr - band * P.band_rows);
@@ -645,6 +696,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       const float ftx0 = (float)fma(t, txd, tx0), fty0 = (float)fma(t, tyd, ty0), fli0 = (float)fma(t, lid, li0);
       const float ftxs = (float)(txd * step), ftys = (float)(tyd * step), flis = (float)(lid * step);
       float jf = 0.0f;
+      if (G > 1) {  // this lane's first sample: gl steps along the exact float64 chain
+        for (int i = 0; i < gl; ++i) t = dadd(t, step);
+        jf = (float)gl;
+      }
       double cr = 0.0, cg = 0.0, cb = 0.0, alpha = 0.0;
       // Front-to-back march (raycaster.py:428-439): the live test precedes
       // each sample, so the sample that crosses the threshold is kept.
@@ -789,6 +844,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
           }
         }
       };
+      if constexpr (G == 1) {
       while (t < t_far && alpha < thresh) {
 #if SBRC_MARCH_PREFETCH
         const double tn = dadd(t, step);
@@ -835,10 +891,77 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         jf += 1.0f;
         ++samples;
       }
+      } else {
+        // Ray group: each lane shades its own samples; the G samples of a
+        // step are then composited in order by every lane of the group with
+        // the reference's live test before each (the same float64 operations
+        // in the same order as the serial loop). Samples a lane computed past
+        // the ray's end are discarded.
+        const unsigned gmask = ((1u << G) - 1u) << (lane & ~(G - 1));
+        bool done = false;
+        while (!done) {
+          double tn = t;
+#pragma unroll
+          for (int i = 0; i < G; ++i) tn = dadd(tn, step);
+          Cell<VT> nxt;
+          bool nxt_in;
+          {
+            const double qx = dadd(P.eye[0], dmul(tn, d[0]));
+            const double qy = dadd(P.eye[1], dmul(tn, d[1]));
+            const double qz = dadd(P.eye[2], dmul(tn, d[2]));
+            nxt_in = in_cube(qx, qy, qz);
+            if (nxt_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, nxt);
+          }
+          const bool have = t < t_far;
+          double sr = 0.0, sg = 0.0, sb = 0.0, sa = 0.0;
+          float fr = 1.0f, fg = 1.0f, fb = 1.0f;
+          if (have) {
+            const double s = cur_in ? cell_combine<VT>(cur, reinterpret_cast<const float*>(u8tab)) : 0.0;
+            const LutPos q = lut_pos(s);
+            const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
+            const double2 b_rg = lut[2 * q.i1], b_ba = lut[2 * q.i1 + 1];
+            sr = dadd(dmul(a_rg.x, q.g), dmul(b_rg.x, q.f));
+            sg = dadd(dmul(a_rg.y, q.g), dmul(b_rg.y, q.f));
+            sb = dadd(dmul(a_ba.x, q.g), dmul(b_ba.x, q.f));
+            sa = dadd(dmul(a_ba.y, q.g), dmul(b_ba.y, q.f));
+            double dfr = 1.0, dfg = 1.0, dfb = 1.0;
+            if (!SKIP || !(q.t <= clear_t)) light_factor(dfr, dfg, dfb);
+            fr = (float)dfr;  // buffer-mode factors are float32 values: exact round trip
+            fg = (float)dfg;
+            fb = (float)dfb;
+          }
+#pragma unroll
+          for (int k = 0; k < G; ++k) {
+            const int src = (lane & ~(G - 1)) + k;
+            const double ksr = __shfl_sync(gmask, sr, src), ksg = __shfl_sync(gmask, sg, src);
+            const double ksb = __shfl_sync(gmask, sb, src), ksa = __shfl_sync(gmask, sa, src);
+            const float kfr = __shfl_sync(gmask, fr, src);
+            const float kfg = white ? kfr : __shfl_sync(gmask, fg, src);
+            const float kfb = white ? kfr : __shfl_sync(gmask, fb, src);
+            const bool khave = __shfl_sync(gmask, (int)have, src) != 0;
+            if (!done) {
+              if (khave && alpha < thresh) {
+                const double one_m = dsub(1.0, alpha);
+                cr = dadd(cr, dmul(dmul(one_m, ksr), (double)kfr));
+                cg = dadd(cg, dmul(dmul(one_m, ksg), (double)kfg));
+                cb = dadd(cb, dmul(dmul(one_m, ksb), (double)kfb));
+                alpha = dadd(alpha, dmul(one_m, ksa));
+                if (gl == 0) ++samples;
+              } else {
+                done = true;
+              }
+            }
+          }
+          t = tn;
+          cur = nxt;
+          cur_in = nxt_in;
+          jf += (float)G;
+        }
+      }
       result = make_float4((float)cr, (float)cg, (float)cb, (float)alpha);
     }
   }
-  if (in_image) {  // background (and padding rows of a partial last band) is transparent black
+  if (in_image && gl == 0) {  // background (and padding rows of a partial last band) is transparent black
     if (P.image != nullptr) reinterpret_cast<float4*>(P.image)[(size_t)lr * P.width + px] = result;
     // fused assembly: the pixel goes straight into every rank's raster image
     // (peer memory over NVLink); a barrier after the kernel completes the frame
@@ -900,34 +1023,36 @@ template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN, bool SKIP>
 void launch_march_skip(const sbrc_render_params& p, cudaStream_t s) {
   sbrc_render_params q = p;
   q.local_rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
-  // latency mode for the default cone kernel when the rank-local image is small
+  // latency mode for the default kernels when the rank-local image is small
   // (A/B in profiles/r01_notes.md: 131K px/rank 1.05 -> 0.75 ms; 262K px: 1.16 vs 1.28)
   constexpr bool LAT = LK == SBRC_LOOKUP_LINEAR &&
                        ((SH == SBRC_SHADE_CONE && CN > 0) ||
                         (SBRC_LATENCY_ALL && ((SH == SBRC_SHADE_SHELL && NS > 0) || SH == SBRC_SHADE_SHADOW)));
-  const bool small = (long long)p.width * q.local_rows <= SBRC_LATENCY_MODE_PIXELS;
-  if (q.tile_counter != nullptr) {  // persistent mode: resident warps pull 8x4 warp tiles
-    const int n_wt = ((p.width + SBRC_TILE_W - 1) / SBRC_TILE_W) *
-                     ((q.local_rows + 32 / SBRC_TILE_W - 1) / (32 / SBRC_TILE_W));
-    if (q.tile_order != nullptr && q.n_tiles != n_wt) q.tile_order = nullptr;  // stale table
+  const MarchShape m = march_shape(q, q.local_rows);
+  const int n_tiles = m.tiles_x * m.tiles_y;
+  if (q.tile_order != nullptr && q.n_tiles != n_tiles) q.tile_order = nullptr;  // stale table
+  constexpr int LG = SBRC_LAT_GROUP;
+  if (m.persistent) {  // resident warps pull 8x4 warp tiles
     cudaMemsetAsync(q.tile_counter, 0, sizeof(unsigned int), s);
-    if (LAT && small) launch_resident(march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4>, 128, n_wt, q, s);
-    else launch_resident(march_kernel<SH, LK, VT, UNIT, NS, CA, CN, SBRC_NARROW_MINB, SKIP, 4>, 128, n_wt, q, s);
+    if (LAT && m.latency) launch_resident(march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4, 1>, 128, n_tiles, q, s);
+    else launch_resident(march_kernel<SH, LK, VT, UNIT, NS, CA, CN, SBRC_NARROW_MINB, SKIP, 4, 1>, 128, n_tiles, q, s);
     return;
   }
-  const bool wide = march_wide(p.width, q.local_rows);
-  const int BW = (wide ? 4 : 2) * SBRC_TILE_W, BH = 2 * (32 / SBRC_TILE_W);
-  dim3 grid((p.width + BW - 1) / BW, (q.local_rows + BH - 1) / BH);
-  if (q.tile_order != nullptr && q.n_tiles != (int)(grid.x * grid.y)) q.tile_order = nullptr;  // stale table
+  const dim3 grid(m.tiles_x, m.tiles_y);
   if constexpr (LAT) {
-    if (small) {
-      if (wide) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 8><<<grid, 256, 0, s>>>(q);
-      else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4><<<grid, 128, 0, s>>>(q);
+    if (m.latency && m.group > 1) {
+      if (m.nw == 8) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 8, LG><<<grid, 256, 0, s>>>(q);
+      else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4, LG><<<grid, 128, 0, s>>>(q);
+      return;
+    }
+    if (m.latency) {
+      if (m.nw == 8) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 8, 1><<<grid, 256, 0, s>>>(q);
+      else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4, 1><<<grid, 128, 0, s>>>(q);
       return;
     }
   }
-  if (wide) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 2, SKIP, 8><<<grid, 256, 0, s>>>(q);
-  else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, SBRC_NARROW_MINB, SKIP, 4><<<grid, 128, 0, s>>>(q);
+  if (m.nw == 8) march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 2, SKIP, 8, 1><<<grid, 256, 0, s>>>(q);
+  else march_kernel<SH, LK, VT, UNIT, NS, CA, CN, SBRC_NARROW_MINB, SKIP, 4, 1><<<grid, 128, 0, s>>>(q);
 }
 
 // skip_clear (a speed hint; results are identical either way) selects the

@@ -250,7 +250,7 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
                   quads_dev: torch.Tensor | None, light_color, voxel_size_max: float,
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
-                  peer_images=(), tile_order: torch.Tensor | None = None,
+                  peer_images=(), heavy_first: bool = False,
                   lut_host: np.ndarray | None = None,
                   tile_counter: torch.Tensor | None = None) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469).
@@ -314,10 +314,11 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     for i, ptr in enumerate(peer_images):
         p.peer_images[i] = int(ptr)
     p.n_peers = len(peer_images)
-    if tile_order is not None:
-        p.tile_order, p.n_tiles = tile_order.data_ptr(), int(tile_order.numel())
     p.sample_count = counter.data_ptr() if counter is not None else None
     p.tile_counter = tile_counter.data_ptr() if tile_counter is not None else None
+    if heavy_first:  # dispatch table over the exact grid sbrc_render will launch
+        order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, N.render_grid(p))
+        p.tile_order, p.n_tiles = order.data_ptr(), int(order.numel())
     return p
 
 
@@ -327,17 +328,18 @@ _ORDER_CACHE: dict = {}
 PERSISTENT_DEFAULT = False
 
 
-def tile_order_for(settings, band_rows: int, rank: int, world: int, device, warp_tiles: bool = False) -> torch.Tensor:
-    """Device copy of the heavy-first dispatch table (schedule.heavy_first), cached per view."""
+def tile_order_for(settings, band_rows: int, rank: int, world: int, device, grid=None) -> torch.Tensor:
+    """Device copy of the heavy-first dispatch table (schedule.heavy_first) over
+    ``grid`` (tiles_x, tiles_y, tile_w, tile_h; default the block grid), cached per view."""
     from .schedule import heavy_first
     cam = settings.camera
     key = (tuple(np.asarray(cam.position, np.float64)), tuple(np.asarray(cam.target, np.float64)),
            tuple(np.asarray(cam.up, np.float64)), float(cam.fov_deg), tuple(settings.viewport), band_rows, rank,
-           world, str(device), warp_tiles)
+           world, str(device), None if grid is None else tuple(grid))
     t = _ORDER_CACHE.get(key)
     if t is None:
         if len(_ORDER_CACHE) > 64:
             _ORDER_CACHE.clear()
-        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world, warp_tiles)).to(device)
+        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world, grid)).to(device)
         _ORDER_CACHE[key] = t
     return t

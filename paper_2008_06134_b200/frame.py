@@ -261,9 +261,7 @@ class FrameRenderer:
                 self.cam.light_color, float(self.dvol.voxel_size.max()), None if p2p else self.chunk, self.counter,
                 band_rows=self.band_rows, rank=self.rank, world=self.world, voxel_size=self.dvol.voxel_size,
                 peer_images=self._peers if p2p else (),
-                tile_order=tile_order_for(self.settings, self.band_rows, self.rank, self.world, self.dev,
-                                          warp_tiles=self.persistent)
-                if (self.world != 2 if self.heavy_first is None else self.heavy_first) else None,
+                heavy_first=self.world != 2 if self.heavy_first is None else self.heavy_first,
                 lut_host=self.lut_host, tile_counter=self.tile_counter)
         self._render_params.sample_count = self.counter.data_ptr() if count_samples else None
         N.check(N.lib.sbrc_render(self._render_params, current_stream_handle()), "sbrc_render")

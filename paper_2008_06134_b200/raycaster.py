@@ -75,8 +75,7 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
     p = render_params(dvol, lut, settings, cam, spec, inten, color, vs, out, counter,
                       band_rows=band_rows, rank=rank, world=world, voxel_size=dvol.voxel_size,
                       peer_images=[int(x.data_ptr()) if isinstance(x, torch.Tensor) else int(x) for x in peer_images],
-                      tile_order=tile_order_for(settings, band_rows, rank, world, dev, warp_tiles=persistent)
-                      if hf else None, lut_host=lut_host, tile_counter=tile_counter)
+                      heavy_first=hf, lut_host=lut_host, tile_counter=tile_counter)
     N.check(N.lib.sbrc_render(p, current_stream_handle()), "sbrc_render")
     img = out[:h] if world == 1 else out
     return (img, counter) if count_samples else img

@@ -18,11 +18,11 @@ from . import _native as N
 from .scene import camera_frame
 
 
-def tile_cost(settings, band_rows: int = 8, rank: int = 0, world: int = 1, warp_tiles: bool = False) -> np.ndarray:
-    """(tiles_y, tiles_x) estimated cost (mean in-cube ray length) of the rank-local K2 tiles
-    (block tiles, or the 8x4 warp tiles of persistent mode)."""
+def tile_cost(settings, band_rows: int = 8, rank: int = 0, world: int = 1, grid=None) -> np.ndarray:
+    """(tiles_y, tiles_x) estimated cost (mean in-cube ray length) of the rank-local K2 tiles of
+    ``grid`` (tiles_x, tiles_y, tile_w, tile_h: N.render_grid of the launch; default the block grid)."""
     w, h = int(settings.viewport[0]), int(settings.viewport[1])
-    tx, ty, bw, bh = N.march_grid(w, h, band_rows if world > 1 else 8, rank, world, warp_tiles)
+    tx, ty, bw, bh = grid if grid is not None else N.march_grid(w, h, band_rows if world > 1 else 8, rank, world)
     fr = camera_frame(settings.camera, settings.viewport)
     eye = np.asarray(settings.camera.position, dtype=np.float64)
     # sample pixels: corners and centre of every tile
@@ -50,7 +50,7 @@ def tile_cost(settings, band_rows: int = 8, rank: int = 0, world: int = 1, warp_
     return np.where(t_out > t_in, t_out - t_in, 0.0).mean(axis=-1)
 
 
-def heavy_first(settings, band_rows: int = 8, rank: int = 0, world: int = 1, warp_tiles: bool = False) -> np.ndarray:
+def heavy_first(settings, band_rows: int = 8, rank: int = 0, world: int = 1, grid=None) -> np.ndarray:
     """int32 dispatch table: tile indices (ty * tiles_x + tx) by decreasing cost."""
-    cost = tile_cost(settings, band_rows, rank, world, warp_tiles).reshape(-1)
+    cost = tile_cost(settings, band_rows, rank, world, grid).reshape(-1)
     return np.argsort(-cost, kind="stable").astype(np.int32)

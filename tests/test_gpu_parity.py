@@ -519,3 +519,37 @@ def test_persistent_march_identical(sb, mode):
                                       persistent=True, heavy_first=hf)
             assert torch.equal(got, ref), (rank, world, hf)
             assert int(n.item()) == int(n_ref.item())
+
+
+@pytest.mark.parametrize("mode", ["sbrc_shadow", "shell", "cone"])
+def test_ray_groups_identical(sb, mode):
+    """Latency-mode ray groups (4 lanes per ray for tiny rank-local images),
+    the single-lane latency kernel and the throughput kernel composite the
+    same float64 operations in the same order: a 320x200 frame (latency mode,
+    one lane per ray), its 4-way band split (16K pixels per rank: ray
+    groups) and the persistent throughput kernel give identical bits and
+    sample counts."""
+    import torch
+    from paper_2008_06134_b200.datasets import make_sphere_blobs
+    v = make_sphere_blobs((48, 48, 48), seed=3)
+    tf = sb.preset("hot")
+    d = (0.3, -0.5, 0.8)
+    settings = sb.RenderSettings(camera=sb.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5)),
+                                 light=sb.Light(direction=d), viewport=(320, 200), step=1 / 128, shading_mode=mode)
+    buf = sb.build_attenuation_buffer(v, tf, sb.LightCamera.fit(d, (1, 1, 1), (64, 64)), sb.make_slice_stack(d, 32))
+    full, n_full = sb.render_device(v, tf, settings, buf, count_samples=True)
+    pers, n_pers = sb.render_device(v, tf, settings, buf, count_samples=True, persistent=True)
+    assert torch.equal(full, pers) and int(n_full.item()) == int(n_pers.item())
+    world, br = 4, 8
+    asm = torch.zeros_like(full)
+    total = 0
+    for r in range(world):
+        part, n = sb.render_device(v, tf, settings, buf, rank=r, world=world, band_rows=br, count_samples=True)
+        total += int(n.item())
+        for lr in range(part.shape[0]):
+            band = lr // br
+            py = (r + band * world) * br + (lr - band * br)
+            if py < full.shape[0]:
+                asm[py] = part[lr]
+    assert torch.equal(asm, full)
+    assert total == int(n_full.item())
