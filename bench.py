@@ -70,8 +70,6 @@ def parse():
     ap.add_argument("--assemble", choices=("p2p", "nccl"), default="p2p",
                     help="N>1 image assembly: fused peer-memory stores from the march kernel (self-checked, "
                          "falls back to NCCL) or NCCL all-gather")
-    ap.add_argument("--march-mode", choices=("auto", "blocks", "persistent"), default="auto",
-                    help="K2 scheduling: one block per tile, or resident warps pulling warp tiles")
     ap.add_argument("--tile-order", choices=("auto", "heavy", "natural"), default="auto")
     ap.add_argument("--raw-voxels", action="store_true",
                     help="u8/u16 volumes: keep the integers in HBM (default: normalised to float32 once)")
@@ -401,8 +399,7 @@ def run_ours(a, cfg, mode):
     vol_gen_s = time.perf_counter() - t0
     fr = FrameRenderer(dvol, tf, cam, spec, settings, build=a.build if world > 1 else "replicated",
                        band_rows=8, device=dev, assemble=a.assemble,
-                       heavy_first={"auto": None, "heavy": True, "natural": False}[a.tile_order],
-                       persistent={"auto": None, "blocks": False, "persistent": True}[a.march_mode])
+                       heavy_first={"auto": None, "heavy": True, "natural": False}[a.tile_order])
     stream = torch.cuda.current_stream()
 
     # samples per frame (deterministic): one counted frame
@@ -527,7 +524,6 @@ def run_ours(a, cfg, mode):
                        "build": a.build if world > 1 else "single", "parallelism": f"image-tiles x{world}",
                        "assemble": fr.assemble_mode if world > 1 else "none",
                        "frame_pipelining": "build(f+1) overlaps march(f)" if pipelined else "off",
-                       "k2_scheduling": "persistent warps, 8x4 warp tiles" if fr.persistent else "one block per tile",
                        "l2": "inputs larger than L2 (volume %d MiB, buffer %d MiB)" % (V >> 20, A >> 20)},
             "gsamples_per_s": samples / (k2_ms * 1e-3) / 1e9,
             "samples_per_frame": samples,

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 5
+#define SBRC_ABI_VERSION 6
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -167,11 +167,6 @@ typedef struct sbrc_render_params {
   int32_t n_tiles;
   const int32_t* tile_order;
   unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
-  /* Persistent mode when non-NULL: the library zeroes this device word, then
-   * launches one resident grid whose warps pull 8x4-pixel warp tiles from it
-   * (atomic counter) until all are rendered — dynamic load balance at warp
-   * granularity instead of the block scheduler's. NULL = one block per tile. */
-  unsigned int* tile_counter;
 } sbrc_render_params;
 
 /* ABI version of the loaded library (== SBRC_ABI_VERSION). */
@@ -269,13 +264,11 @@ int sbrc_ipc_close(void* ptr);
 int sbrc_march_grid(int width, int height, int band_rows, int rank, int world, int grid[4]);
 
 /* The tile grid sbrc_render will launch for *p (block shape, latency mode,
- * ray groups and persistent mode all depend on the params): grid[0..3] =
+ * and ray groups depend on the params): grid[0..3] =
  * tiles_x, tiles_y, tile width and height in pixels. tile_order tables must
  * index this grid. */
 int sbrc_render_grid(const sbrc_render_params* p, int grid[4]);
 
-/* The same for persistent mode (tile_counter set): warp tiles of 8 x 4 pixels. */
-int sbrc_march_warp_grid(int width, int height, int band_rows, int rank, int world, int grid[4]);
 
 /* Number of rank-local image rows sbrc_render writes for (height, band_rows, rank, world). */
 int sbrc_local_rows(int height, int band_rows, int rank, int world);

@@ -16,7 +16,7 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 MAX_PEERS = 8
@@ -31,7 +31,7 @@ EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume
            "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_shadow_oracle", "sbrc_light_factor",
            "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_ipc_alloc", "sbrc_ipc_free", "sbrc_ipc_handle",
            "sbrc_ipc_open", "sbrc_ipc_close", "sbrc_march_grid", "sbrc_local_rows",
-           "sbrc_march_warp_grid", "sbrc_render_grid")
+           "sbrc_render_grid")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -71,8 +71,7 @@ class SbrcRenderParams(C.Structure):
                 ("band_rows", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("local_rows", C.c_int32),
                 ("scene_light_dir", D3), ("phong", C.c_double * 4), ("voxel_size", D3),
                 ("image", C.c_void_p), ("peer_images", C.c_void_p * MAX_PEERS), ("n_peers", C.c_int32),
-                ("n_tiles", C.c_int32), ("tile_order", C.c_void_p), ("sample_count", C.c_void_p),
-                ("tile_counter", C.c_void_p)]
+                ("n_tiles", C.c_int32), ("tile_order", C.c_void_p), ("sample_count", C.c_void_p)]
 
 
 class SbrcHalfAngleParams(C.Structure):
@@ -102,7 +101,6 @@ def _load() -> C.CDLL:
     lib.sbrc_render.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p]
     lib.sbrc_local_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
     lib.sbrc_march_grid.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int * 4]
-    lib.sbrc_march_warp_grid.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int * 4]
     lib.sbrc_render_grid.argtypes = [C.POINTER(SbrcRenderParams), C.c_int * 4]
     lib.sbrc_light_factor.argtypes = [C.POINTER(SbrcRenderParams), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
@@ -154,11 +152,8 @@ def render_grid(p) -> tuple[int, int, int, int]:
     return g[0], g[1], g[2], g[3]
 
 
-def march_grid(width: int, height: int, band_rows: int, rank: int, world: int,
-               warp_tiles: bool = False) -> tuple[int, int, int, int]:
-    """(tiles_x, tiles_y, tile_w, tile_h) of K2's block grid, or of its warp
-    tiles (persistent mode)."""
+def march_grid(width: int, height: int, band_rows: int, rank: int, world: int) -> tuple[int, int, int, int]:
+    """(tiles_x, tiles_y, tile_w, tile_h) of the throughput K2 block grid."""
     g = (C.c_int * 4)()
-    fn = lib.sbrc_march_warp_grid if warp_tiles else lib.sbrc_march_grid
-    check(fn(width, height, band_rows, rank, world, g), "sbrc_march_grid")
+    check(lib.sbrc_march_grid(width, height, band_rows, rank, world, g), "sbrc_march_grid")
     return g[0], g[1], g[2], g[3]

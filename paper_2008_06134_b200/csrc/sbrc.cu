@@ -443,17 +443,6 @@ int sbrc_render_grid(const sbrc_render_params* p, int* grid) {
   return SBRC_OK;
 }
 
-int sbrc_march_warp_grid(int width, int height, int band_rows, int rank, int world, int* grid) {
-  if (grid == nullptr) return SBRC_EINVAL;
-  const int rows = sbrc_local_rows(height, band_rows, rank, world);
-  constexpr int TW = SBRC_TILE_W, TH = 32 / SBRC_TILE_W;
-  grid[0] = (width + TW - 1) / TW;
-  grid[1] = (rows + TH - 1) / TH;
-  grid[2] = TW;
-  grid[3] = TH;
-  return SBRC_OK;
-}
-
 int sbrc_local_rows(int height, int band_rows, int rank, int world) {
   if (height < 1 || band_rows < 1 || world < 1 || rank < 0 || rank >= world) return 0;
   const int bands = (height + band_rows - 1) / band_rows;

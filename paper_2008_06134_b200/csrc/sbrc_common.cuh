@@ -453,25 +453,17 @@ inline bool march_latency_kernel(const sbrc_render_params& p) {
 // The K2 launch shape for these params: the one rule the launch and
 // sbrc_render_grid (heavy-first tables on the host) share.
 struct MarchShape {
-  bool persistent, latency;
+  bool latency;
   int nw, group, bw, bh, tiles_x, tiles_y;
 };
 inline MarchShape march_shape(const sbrc_render_params& p, int local_rows) {
   MarchShape m{};
-  m.persistent = p.tile_counter != nullptr;
   m.latency = march_latency_kernel(p) && (long long)p.width * local_rows <= SBRC_LATENCY_MODE_PIXELS;
-  if (m.persistent) {  // warp tiles
-    m.nw = 4;
-    m.group = 1;
-    m.bw = SBRC_TILE_W;
-    m.bh = 32 / SBRC_TILE_W;
-  } else {
-    m.nw = march_wide(p.width, local_rows) ? 8 : 4;
-    m.group = m.latency && (long long)p.width * local_rows <= SBRC_GROUP_PIXELS ? SBRC_LAT_GROUP : 1;
-    const int tw = m.group == 1 ? SBRC_TILE_W : 4, th = (32 / m.group) / tw;
-    m.bw = (m.nw / 2) * tw;
-    m.bh = 2 * th;
-  }
+  m.nw = march_wide(p.width, local_rows) ? 8 : 4;
+  m.group = m.latency && (long long)p.width * local_rows <= SBRC_GROUP_PIXELS ? SBRC_LAT_GROUP : 1;
+  const int tw = m.group == 1 ? SBRC_TILE_W : 4, th = (32 / m.group) / tw;
+  m.bw = (m.nw / 2) * tw;
+  m.bh = 2 * th;
   m.tiles_x = (p.width + m.bw - 1) / m.bw;
   m.tiles_y = (local_rows + m.bh - 1) / m.bh;
   return m;
@@ -558,43 +550,25 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
   // Pixel of this lane: each warp owns a TW x TH pixel tile, a block WX x 2
   // warp tiles. Ray groups (G > 1): G adjacent lanes share one ray and take
   // its samples round-robin (lane gl: samples gl, gl+G, ...), so a long ray
-  // runs G samples per serial step; warps then own 32/G rays. Persistent
-  // mode (tile_counter set, G == 1): each warp pulls warp tiles from the
-  // counter until none are left.
+  // runs G samples per serial step; warps then own 32/G rays.
   constexpr int TW = G == 1 ? SBRC_TILE_W : 4, TH = (32 / G) / TW;
   constexpr int WX = NW / 2, WY = 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ray = lane / G, gl = lane % G;
-  const bool persistent = P.tile_counter != nullptr;
-  const int wtx = (P.width + TW - 1) / TW;
-  const int n_wt = wtx * ((P.local_rows + TH - 1) / TH);
-  unsigned int samples = 0;
-  for (int iter = 0;; ++iter) {
-  int px, lr;
-  if (persistent) {
-    int wt = 0;
-    if (lane == 0) wt = (int)atomicAdd(P.tile_counter, 1u);
-    wt = __shfl_sync(0xffffffffu, wt, 0);
-    if (wt >= n_wt) break;
-    if (P.tile_order != nullptr) wt = __ldg(P.tile_order + wt);
-    px = (wt % wtx) * TW + (ray % TW);
-    lr = (wt / wtx) * TH + (ray / TW);
-  } else {
-    if (iter > 0) break;
-    int bx = blockIdx.x, by = blockIdx.y;
-    if (P.tile_order != nullptr) {  // heavy-first dispatch: this block renders tile tile_order[b]
-      const int t = __ldg(P.tile_order + blockIdx.y * gridDim.x + blockIdx.x);
-      bx = t % gridDim.x;
-      by = t / gridDim.x;
-    }
-    px = bx * (WX * TW) + (warp % WX) * TW + (ray % TW);
-    lr = by * (WY * TH) + (warp / WX) * TH + (ray / TW);  // rank-local row
+  int bx = blockIdx.x, by = blockIdx.y;
+  if (P.tile_order != nullptr) {  // heavy-first dispatch: this block renders tile tile_order[b]
+    const int t = __ldg(P.tile_order + blockIdx.y * gridDim.x + blockIdx.x);
+    bx = t % gridDim.x;
+    by = t / gridDim.x;
   }
+  const int px = bx * (WX * TW) + (warp % WX) * TW + (ray % TW);
+  const int lr = by * (WY * TH) + (warp / WX) * TH + (ray / TW);  // rank-local row
   const int band = lr / P.band_rows;
   const int py = (P.rank + band * P.world) * P.band_rows + (lr - band * P.band_rows);
   const bool in_image = px < P.width && lr < P.local_rows;
   const bool valid = in_image && py < P.height;
 
+  unsigned int samples = 0;
   float4 result = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
     // ---- Camera.rays (raycaster.py:53-68), numpy op order, float64.
@@ -969,7 +943,6 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       for (int i = 0; i < P.n_peers; ++i)
         reinterpret_cast<float4*>(P.peer_images[i])[(size_t)py * P.width + px] = result;
   }
-  }  // tile loop
   if (P.n_peers > 0) __threadfence_system();
   if (P.sample_count != nullptr) {
     const unsigned int tot = __reduce_add_sync(0xffffffffu, samples);
@@ -1006,19 +979,6 @@ inline bool unit_box(const sbrc_volume& v) {
   return true;
 }
 
-// One resident grid (persistent mode): as many blocks as fit on the device
-// at once, capped by the work (warp tiles / warps per block).
-template <typename Kernel>
-void launch_resident(Kernel kernel, int threads, int n_wt, const sbrc_render_params& q, cudaStream_t s) {
-  int dev = 0, sms = SBRC_SM_COUNT, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
-  const int warps = threads / 32;
-  const int blocks = max(1, min(sms * max(per_sm, 1), (n_wt + warps - 1) / warps));
-  kernel<<<blocks, threads, 0, s>>>(q);
-}
-
 template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN, bool SKIP>
 void launch_march_skip(const sbrc_render_params& p, cudaStream_t s) {
   sbrc_render_params q = p;
@@ -1032,12 +992,6 @@ void launch_march_skip(const sbrc_render_params& p, cudaStream_t s) {
   const int n_tiles = m.tiles_x * m.tiles_y;
   if (q.tile_order != nullptr && q.n_tiles != n_tiles) q.tile_order = nullptr;  // stale table
   constexpr int LG = SBRC_LAT_GROUP;
-  if (m.persistent) {  // resident warps pull 8x4 warp tiles
-    cudaMemsetAsync(q.tile_counter, 0, sizeof(unsigned int), s);
-    if (LAT && m.latency) launch_resident(march_kernel<SH, LK, VT, UNIT, NS, CA, CN, 1, SKIP, 4, 1>, 128, n_tiles, q, s);
-    else launch_resident(march_kernel<SH, LK, VT, UNIT, NS, CA, CN, SBRC_NARROW_MINB, SKIP, 4, 1>, 128, n_tiles, q, s);
-    return;
-  }
   const dim3 grid(m.tiles_x, m.tiles_y);
   if constexpr (LAT) {
     if (m.latency && m.group > 1) {

@@ -251,8 +251,7 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
                   peer_images=(), heavy_first: bool = False,
-                  lut_host: np.ndarray | None = None,
-                  tile_counter: torch.Tensor | None = None) -> N.SbrcRenderParams:
+                  lut_host: np.ndarray | None = None) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469).
     ``lut_host`` (the resolved LUT on the host) enables the skip_clear hint."""
     mode = settings.shading_mode
@@ -315,7 +314,6 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
         p.peer_images[i] = int(ptr)
     p.n_peers = len(peer_images)
     p.sample_count = counter.data_ptr() if counter is not None else None
-    p.tile_counter = tile_counter.data_ptr() if tile_counter is not None else None
     if heavy_first:  # dispatch table over the exact grid sbrc_render will launch
         order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, N.render_grid(p))
         p.tile_order, p.n_tiles = order.data_ptr(), int(order.numel())
@@ -323,9 +321,6 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
 
 
 _ORDER_CACHE: dict = {}
-
-#: K2 persistent mode (resident warps pulling 8x4 warp tiles; sbrc_render_params.tile_counter) by default
-PERSISTENT_DEFAULT = False
 
 
 def tile_order_for(settings, band_rows: int, rank: int, world: int, device, grid=None) -> torch.Tensor:

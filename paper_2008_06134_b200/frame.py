@@ -108,7 +108,7 @@ class FrameRenderer:
 
     def __init__(self, volume, tf, light_cam, spec, settings, *, group=None, build: str = "replicated",
                  band_rows: int = 8, compensation_n: float = 0.0, device=None, assemble: str = "nccl",
-                 heavy_first: bool | None = None, persistent: bool | None = None):
+                 heavy_first: bool | None = None):
         check_frame(light_cam, spec)
         if build not in ("replicated", "sharded"):
             raise ValueError(f"build must be 'replicated' or 'sharded', got {build!r}")
@@ -123,13 +123,10 @@ class FrameRenderer:
         self.tf, self.settings, self.build_mode = tf, settings, build
         # heavy-first dispatch (schedule.py) measured: +1% at 1 rank, +8% at 4, +14% at 8, -6% at 2
         self.heavy_first = heavy_first
-        from . import device as _device
-        self.persistent = _device.PERSISTENT_DEFAULT if persistent is None else persistent
         self.band_rows, self.comp = band_rows, compensation_n
         self.lut_host = tf.resolve(settings.step)
         self.lut = f64_tensor(self.lut_host, self.dev)
         self.counter = torch.zeros(1, dtype=torch.int64, device=self.dev)
-        self.tile_counter = torch.zeros(1, dtype=torch.int32, device=self.dev) if self.persistent else None
         w, h = int(settings.viewport[0]), int(settings.viewport[1])
         self.width, self.height = w, h
         self.rows_local, perm = band_layout(h, band_rows, self.world)
@@ -262,7 +259,7 @@ class FrameRenderer:
                 band_rows=self.band_rows, rank=self.rank, world=self.world, voxel_size=self.dvol.voxel_size,
                 peer_images=self._peers if p2p else (),
                 heavy_first=self.world != 2 if self.heavy_first is None else self.heavy_first,
-                lut_host=self.lut_host, tile_counter=self.tile_counter)
+                lut_host=self.lut_host)
         self._render_params.sample_count = self.counter.data_ptr() if count_samples else None
         N.check(N.lib.sbrc_render(self._render_params, current_stream_handle()), "sbrc_render")
 

@@ -39,7 +39,7 @@ def _quads_of(buffer, dev) -> torch.Tensor:
 
 def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: bool = False,
                   rank: int = 0, world: int = 1, band_rows: int = 8, out: torch.Tensor | None = None,
-                  peer_images=(), heavy_first: bool | None = None, persistent: bool | None = None):
+                  peer_images=(), heavy_first: bool | None = None):
     """Enqueue K2; returns the (rows, W, 4) CUDA image (all rows when world == 1)
     and, with ``count_samples``, a 1-element int64 CUDA tensor of executed samples."""
     mode = settings.shading_mode
@@ -68,14 +68,11 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
         if (n, hh, ww) != (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0])):
             raise ValueError("attenuation intensity shape does not match its camera/stack")
     vs = float(dvol.voxel_size.max())   # ShellKernel.default(v.voxel_size.max()), :403
-    from . import device as _device
-    persistent = _device.PERSISTENT_DEFAULT if persistent is None else persistent
     hf = (world != 2) if heavy_first is None else heavy_first
-    tile_counter = torch.empty(1, dtype=torch.int32, device=dev) if persistent else None
     p = render_params(dvol, lut, settings, cam, spec, inten, color, vs, out, counter,
                       band_rows=band_rows, rank=rank, world=world, voxel_size=dvol.voxel_size,
                       peer_images=[int(x.data_ptr()) if isinstance(x, torch.Tensor) else int(x) for x in peer_images],
-                      heavy_first=hf, lut_host=lut_host, tile_counter=tile_counter)
+                      heavy_first=hf, lut_host=lut_host)
     N.check(N.lib.sbrc_render(p, current_stream_handle()), "sbrc_render")
     img = out[:h] if world == 1 else out
     return (img, counter) if count_samples else img

@@ -19,13 +19,11 @@ def main():
     buf = sb.build_attenuation_buffer(dvol, tf, cam, spec)
     band = int(sys.argv[1]) if len(sys.argv) > 1 else 8
     hf = {"hf": True, "nohf": False}.get(sys.argv[2]) if len(sys.argv) > 2 else None  # None: library default
-    persistent = {"persist": True, "blocks": False}.get(sys.argv[3]) if len(sys.argv) > 3 else None
     out = {}
     for world in (1, 2, 4, 8):
         br = band if band > 0 else -(-(settings.viewport[1] // world) // 8) * 8  # 0: contiguous blocks
         for r in range(3):
-            sb.render_device(dvol, tf, settings, buf, rank=0, world=world, band_rows=br, heavy_first=hf,
-                                 persistent=persistent)
+            sb.render_device(dvol, tf, settings, buf, rank=0, world=world, band_rows=br, heavy_first=hf)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ranks = range(world)
@@ -33,8 +31,7 @@ def main():
         for rank in ranks:  # every rank's share, one after the other
             e0.record()
             for _ in range(5):
-                sb.render_device(dvol, tf, settings, buf, rank=rank, world=world, band_rows=br, heavy_first=hf,
-                                 persistent=persistent)
+                sb.render_device(dvol, tf, settings, buf, rank=rank, world=world, band_rows=br, heavy_first=hf)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 5)

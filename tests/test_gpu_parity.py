@@ -496,38 +496,13 @@ def test_zero_emission_skip_identical(sb, mode, monkeypatch):
     assert imgs[0][..., 3].max() > 0.1  # something was rendered
 
 
-@pytest.mark.parametrize("mode", ["none", "sbrc_shadow", "shell", "cone"])
-def test_persistent_march_identical(sb, mode):
-    """Persistent K2 (resident warps pulling 8x4 warp tiles from a counter,
-    natural or heavy-first order) renders the same bits and the same sample
-    count as one block per tile, for a full frame and a rank's share."""
-    import torch
-    from paper_2008_06134_b200.datasets import make_sphere_blobs
-    v = make_sphere_blobs((40, 40, 40), seed=7)
-    tf = sb.preset("hot")
-    d = (0.3, -0.5, 0.8)
-    settings = sb.RenderSettings(camera=sb.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5)),
-                                 light=sb.Light(direction=d), viewport=(100, 72), step=1 / 96, shading_mode=mode)
-    buf = None
-    if mode != "none":
-        buf = sb.build_attenuation_buffer(v, tf, sb.LightCamera.fit(d, (1, 1, 1), (48, 48)), sb.make_slice_stack(d, 24))
-    for rank, world in ((0, 1), (1, 3)):
-        ref, n_ref = sb.render_device(v, tf, settings, buf, rank=rank, world=world, count_samples=True,
-                                      persistent=False, heavy_first=False)
-        for hf in (False, True):
-            got, n = sb.render_device(v, tf, settings, buf, rank=rank, world=world, count_samples=True,
-                                      persistent=True, heavy_first=hf)
-            assert torch.equal(got, ref), (rank, world, hf)
-            assert int(n.item()) == int(n_ref.item())
-
-
 @pytest.mark.parametrize("mode", ["sbrc_shadow", "shell", "cone"])
 def test_ray_groups_identical(sb, mode):
-    """Latency-mode ray groups (4 lanes per ray for tiny rank-local images),
-    the single-lane latency kernel and the throughput kernel composite the
-    same float64 operations in the same order: a 320x200 frame (latency mode,
-    one lane per ray), its 4-way band split (16K pixels per rank: ray
-    groups) and the persistent throughput kernel give identical bits and
+    """The throughput kernel, the latency kernel (one lane per ray) and ray
+    groups (4 lanes per ray, tiny rank-local images) composite the same
+    float64 operations in the same order: a 640x400 frame (throughput
+    kernel), its 2-way band split (128K pixels per rank: latency kernel) and
+    its 8-way split (32K pixels per rank: ray groups) give identical bits and
     sample counts."""
     import torch
     from paper_2008_06134_b200.datasets import make_sphere_blobs
@@ -535,21 +510,20 @@ def test_ray_groups_identical(sb, mode):
     tf = sb.preset("hot")
     d = (0.3, -0.5, 0.8)
     settings = sb.RenderSettings(camera=sb.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5)),
-                                 light=sb.Light(direction=d), viewport=(320, 200), step=1 / 128, shading_mode=mode)
+                                 light=sb.Light(direction=d), viewport=(640, 400), step=1 / 128, shading_mode=mode)
     buf = sb.build_attenuation_buffer(v, tf, sb.LightCamera.fit(d, (1, 1, 1), (64, 64)), sb.make_slice_stack(d, 32))
     full, n_full = sb.render_device(v, tf, settings, buf, count_samples=True)
-    pers, n_pers = sb.render_device(v, tf, settings, buf, count_samples=True, persistent=True)
-    assert torch.equal(full, pers) and int(n_full.item()) == int(n_pers.item())
-    world, br = 4, 8
-    asm = torch.zeros_like(full)
-    total = 0
-    for r in range(world):
-        part, n = sb.render_device(v, tf, settings, buf, rank=r, world=world, band_rows=br, count_samples=True)
-        total += int(n.item())
-        for lr in range(part.shape[0]):
-            band = lr // br
-            py = (r + band * world) * br + (lr - band * br)
-            if py < full.shape[0]:
-                asm[py] = part[lr]
-    assert torch.equal(asm, full)
-    assert total == int(n_full.item())
+    br = 8
+    for world in (2, 8):
+        asm = torch.zeros_like(full)
+        total = 0
+        for r in range(world):
+            part, n = sb.render_device(v, tf, settings, buf, rank=r, world=world, band_rows=br, count_samples=True)
+            total += int(n.item())
+            for lr in range(part.shape[0]):
+                band = lr // br
+                py = (r + band * world) * br + (lr - band * br)
+                if py < full.shape[0]:
+                    asm[py] = part[lr]
+        assert torch.equal(asm, full), world
+        assert total == int(n_full.item())
