@@ -421,9 +421,6 @@ struct ShellTap {
 #ifndef SBRC_TILE_W
 #define SBRC_TILE_W 8  // warp pixel tile width (8 x 4)
 #endif
-#ifndef SBRC_MARCH_PREFETCH
-#define SBRC_MARCH_PREFETCH 1
-#endif
 #ifndef SBRC_SKIP_CLEAR
 #define SBRC_SKIP_CLEAR 1  // instantiate the zero-emission skip (sbrc_render_params.skip_clear)
 #endif
@@ -480,7 +477,6 @@ template <int SHADING, int LOOKUP, int VT, bool UNIT, int NSHELL, int CONE_A, in
 __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_params P) {
   static_assert(G == 1 || SHADING == SBRC_SHADE_SHADOW || SHADING == SBRC_SHADE_SHELL || SHADING == SBRC_SHADE_CONE,
                 "ray groups carry float32 light factors (buffer modes)");
-  static_assert(G == 1 || SBRC_MARCH_PREFETCH, "ray groups use the prefetched cell");
   __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
@@ -677,7 +673,6 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       double cr = 0.0, cg = 0.0, cb = 0.0, alpha = 0.0;
       // Front-to-back march (raycaster.py:428-439): the live test precedes
       // each sample, so the sample that crosses the threshold is kept.
-#if SBRC_MARCH_PREFETCH
       // the voxel cell of sample j+1 is gathered while sample j is shaded
       // (harmless past the exit: outside the cube nothing is fetched)
       Cell<VT> cur;
@@ -689,7 +684,6 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         cur_in = in_cube(qx, qy, qz);
         if (cur_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, cur);
       }
-#endif
       // Light factor of the sample at t (sample counter jf).
       auto light_factor = [&](double& fr, double& fg, double& fb) {
         if (SHADING == SBRC_SHADE_PHONG || SHADING == SBRC_SHADE_EXTINCTION) {
@@ -819,25 +813,18 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         }
       };
       if constexpr (G == 1) {
-      while (t < t_far && alpha < thresh) {
-#if SBRC_MARCH_PREFETCH
+      // One sample: shade the prefetched cell `use` while the next sample's
+      // cell is gathered into `fill`.
+      auto sample = [&](const Cell<VT>& use, const bool use_in, Cell<VT>& fill, bool& fill_in) {
         const double tn = dadd(t, step);
-        Cell<VT> nxt;
-        bool nxt_in;
         {
           const double qx = dadd(P.eye[0], dmul(tn, d[0]));
           const double qy = dadd(P.eye[1], dmul(tn, d[1]));
           const double qz = dadd(P.eye[2], dmul(tn, d[2]));
-          nxt_in = in_cube(qx, qy, qz);
-          if (nxt_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, nxt);
+          fill_in = in_cube(qx, qy, qz);
+          if (fill_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, fill);
         }
-        const double s = cur_in ? cell_combine<VT>(cur, reinterpret_cast<const float*>(u8tab)) : 0.0;
-#else
-        const double qx = dadd(P.eye[0], dmul(t, d[0]));
-        const double qy = dadd(P.eye[1], dmul(t, d[1]));
-        const double qz = dadd(P.eye[2], dmul(t, d[2]));
-        const double s = trilinear64<VT, UNIT>(P.volume, reinterpret_cast<const float*>(u8tab), qx, qy, qz);
-#endif
+        const double s = use_in ? cell_combine<VT>(use, reinterpret_cast<const float*>(u8tab)) : 0.0;
         const LutPos q = lut_pos(s);
         const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
         const double2 b_rg = lut[2 * q.i1], b_ba = lut[2 * q.i1 + 1];
@@ -855,15 +842,16 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         cg = dadd(cg, dmul(dmul(one_m, sg), fg));
         cb = dadd(cb, dmul(dmul(one_m, sb), fb));
         alpha = dadd(alpha, dmul(one_m, sa));
-#if SBRC_MARCH_PREFETCH
         t = tn;
-        cur = nxt;
-        cur_in = nxt_in;
-#else
-        t = dadd(t, step);
-#endif
         jf += 1.0f;
         ++samples;
+      };
+      while (t < t_far && alpha < thresh) {
+        Cell<VT> nxt;
+        bool nxt_in;
+        sample(cur, cur_in, nxt, nxt_in);
+        cur = nxt;
+        cur_in = nxt_in;
       }
       } else {
         // Ray group: each lane shades its own samples; the G samples of a
