@@ -70,7 +70,9 @@ def parse():
     ap.add_argument("--assemble", choices=("p2p", "nccl"), default="p2p",
                     help="N>1 image assembly: fused peer-memory stores from the march kernel (self-checked, "
                          "falls back to NCCL) or NCCL all-gather")
-    ap.add_argument("--tile-order", choices=("auto", "heavy", "natural"), default="auto")
+    ap.add_argument("--tile-order", choices=("auto", "heavy", "natural", "measured"), default="auto",
+                    help="K2 dispatch order: heavy-first by ray length, natural, or heavy-first by the previous "
+                         "frame's measured tile costs; auto = measured with > 1 rank, ray length at 1")
     ap.add_argument("--raw-voxels", action="store_true",
                     help="u8/u16 volumes: keep the integers in HBM (default: normalised to float32 once)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -399,7 +401,8 @@ def run_ours(a, cfg, mode):
     vol_gen_s = time.perf_counter() - t0
     fr = FrameRenderer(dvol, tf, cam, spec, settings, build=a.build if world > 1 else "replicated",
                        band_rows=8, device=dev, assemble=a.assemble,
-                       heavy_first={"auto": None, "heavy": True, "natural": False}[a.tile_order])
+                       heavy_first={"auto": None, "heavy": True, "natural": False, "measured": True}[a.tile_order],
+                       feedback={"auto": None, "heavy": False, "natural": False, "measured": True}[a.tile_order])
     stream = torch.cuda.current_stream()
 
     # samples per frame (deterministic): one counted frame
@@ -524,6 +527,8 @@ def run_ours(a, cfg, mode):
                        "build": a.build if world > 1 else "single", "parallelism": f"image-tiles x{world}",
                        "assemble": fr.assemble_mode if world > 1 else "none",
                        "frame_pipelining": "build(f+1) overlaps march(f)" if pipelined else "off",
+                       "tile_order": "measured (previous frame)" if fr.feedback is not None else
+                       ("ray length" if (fr.world != 2 if fr.heavy_first is None else fr.heavy_first) else "natural"),
                        "l2": "inputs larger than L2 (volume %d MiB, buffer %d MiB)" % (V >> 20, A >> 20)},
             "gsamples_per_s": samples / (k2_ms * 1e-3) / 1e9,
             "samples_per_frame": samples,

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 6
+#define SBRC_ABI_VERSION 7
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -167,6 +167,11 @@ typedef struct sbrc_render_params {
   int32_t n_tiles;
   const int32_t* tile_order;
   unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
+  /* Optional measured tile costs (n_tiles entries over the sbrc_render_grid
+   * tiles, zeroed by the caller): each block atomically maxes the executed
+   * sample count of its longest ray into tile_steps[tile]. Sorted in
+   * decreasing order it is the next frame's heavy-first tile_order. */
+  unsigned int* tile_steps;
 } sbrc_render_params;
 
 /* ABI version of the loaded library (== SBRC_ABI_VERSION). */

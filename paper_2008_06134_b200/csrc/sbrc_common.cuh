@@ -936,6 +936,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
     const unsigned int tot = __reduce_add_sync(0xffffffffu, samples);
     if (lane == 0 && tot) atomicAdd(P.sample_count, (unsigned long long)tot);
   }
+  if (P.tile_steps != nullptr) {  // measured cost of this tile: its longest ray's sample count
+    const unsigned int mx = __reduce_max_sync(0xffffffffu, samples);
+    if (lane == 0 && mx) atomicMax(P.tile_steps + (by * gridDim.x + bx), mx);
+  }
 }
 
 // ---------------------------------------------------------------- dispatch

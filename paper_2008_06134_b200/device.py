@@ -251,7 +251,7 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
                   peer_images=(), heavy_first: bool = False,
-                  lut_host: np.ndarray | None = None) -> N.SbrcRenderParams:
+                  lut_host: np.ndarray | None = None, feedback=None) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469).
     ``lut_host`` (the resolved LUT on the host) enables the skip_clear hint."""
     mode = settings.shading_mode
@@ -315,7 +315,11 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     p.n_peers = len(peer_images)
     p.sample_count = counter.data_ptr() if counter is not None else None
     if heavy_first:  # dispatch table over the exact grid sbrc_render will launch
-        order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, N.render_grid(p))
+        grid = N.render_grid(p)
+        order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, grid)
+        if feedback is not None:  # measured order of the previous frame (schedule.TileFeedback)
+            order, steps = feedback.prepare(grid, order)
+            p.tile_steps = steps.data_ptr()
         p.tile_order, p.n_tiles = order.data_ptr(), int(order.numel())
     return p
 

@@ -108,7 +108,7 @@ class FrameRenderer:
 
     def __init__(self, volume, tf, light_cam, spec, settings, *, group=None, build: str = "replicated",
                  band_rows: int = 8, compensation_n: float = 0.0, device=None, assemble: str = "nccl",
-                 heavy_first: bool | None = None):
+                 heavy_first: bool | None = None, feedback: bool | None = None):
         check_frame(light_cam, spec)
         if build not in ("replicated", "sharded"):
             raise ValueError(f"build must be 'replicated' or 'sharded', got {build!r}")
@@ -123,6 +123,13 @@ class FrameRenderer:
         self.tf, self.settings, self.build_mode = tf, settings, build
         # heavy-first dispatch (schedule.py) measured: +1% at 1 rank, +8% at 4, +14% at 8, -6% at 2
         self.heavy_first = heavy_first
+        # heavy-first by the previous frame's measured tile costs (schedule.TileFeedback):
+        # default with > 1 rank (rank shares at 2/4/8 ranks: 2.34/1.17/0.76 -> 1.63/0.90/0.62 ms
+        # vs the geometric estimate); at 1 rank the geometric order keeps better locality
+        from .schedule import TileFeedback
+        if feedback is None:
+            feedback = self.world > 1 and heavy_first is not False
+        self.feedback = TileFeedback() if feedback else None
         self.band_rows, self.comp = band_rows, compensation_n
         self.lut_host = tf.resolve(settings.step)
         self.lut = f64_tensor(self.lut_host, self.dev)
@@ -258,10 +265,15 @@ class FrameRenderer:
                 self.cam.light_color, float(self.dvol.voxel_size.max()), None if p2p else self.chunk, self.counter,
                 band_rows=self.band_rows, rank=self.rank, world=self.world, voxel_size=self.dvol.voxel_size,
                 peer_images=self._peers if p2p else (),
-                heavy_first=self.world != 2 if self.heavy_first is None else self.heavy_first,
-                lut_host=self.lut_host)
+                heavy_first=(self.feedback is not None or self.world != 2) if self.heavy_first is None
+                else self.heavy_first,
+                lut_host=self.lut_host, feedback=self.feedback)
+        elif self.feedback is not None and self.feedback.steps is not None:
+            self.feedback.steps.zero_()
         self._render_params.sample_count = self.counter.data_ptr() if count_samples else None
         N.check(N.lib.sbrc_render(self._render_params, current_stream_handle()), "sbrc_render")
+        if self.feedback is not None:
+            self.feedback.update()
 
     def assemble(self) -> torch.Tensor:
         if self.world > 1:

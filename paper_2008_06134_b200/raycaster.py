@@ -39,7 +39,7 @@ def _quads_of(buffer, dev) -> torch.Tensor:
 
 def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: bool = False,
                   rank: int = 0, world: int = 1, band_rows: int = 8, out: torch.Tensor | None = None,
-                  peer_images=(), heavy_first: bool | None = None):
+                  peer_images=(), heavy_first: bool | None = None, feedback=None):
     """Enqueue K2; returns the (rows, W, 4) CUDA image (all rows when world == 1)
     and, with ``count_samples``, a 1-element int64 CUDA tensor of executed samples."""
     mode = settings.shading_mode
@@ -72,8 +72,10 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
     p = render_params(dvol, lut, settings, cam, spec, inten, color, vs, out, counter,
                       band_rows=band_rows, rank=rank, world=world, voxel_size=dvol.voxel_size,
                       peer_images=[int(x.data_ptr()) if isinstance(x, torch.Tensor) else int(x) for x in peer_images],
-                      heavy_first=hf, lut_host=lut_host)
+                      heavy_first=hf, lut_host=lut_host, feedback=feedback if hf else None)
     N.check(N.lib.sbrc_render(p, current_stream_handle()), "sbrc_render")
+    if feedback is not None and hf:
+        feedback.update()
     img = out[:h] if world == 1 else out
     return (img, counter) if count_samples else img
 

@@ -14,6 +14,8 @@ from __future__ import annotations
 
 import numpy as np
 
+import torch
+
 from . import _native as N
 from .scene import camera_frame
 
@@ -54,3 +56,33 @@ def heavy_first(settings, band_rows: int = 8, rank: int = 0, world: int = 1, gri
     """int32 dispatch table: tile indices (ty * tiles_x + tx) by decreasing cost."""
     cost = tile_cost(settings, band_rows, rank, world, grid).reshape(-1)
     return np.argsort(-cost, kind="stable").astype(np.int32)
+
+
+class TileFeedback:
+    """Heavy-first order from measured costs. K2 writes each tile's longest-ray
+    sample count (``sbrc_render_params.tile_steps``); after the launch the
+    tiles are sorted by it on the device, and the next frame of the same view
+    dispatches in that order (the first frame uses the geometric estimate).
+    Everything stays on the launching stream: no host round trip."""
+
+    def __init__(self):
+        self.grid = None
+        self.order = None
+        self.steps = None
+
+    def prepare(self, grid, initial_order: torch.Tensor):
+        """(order, steps) device tensors for a launch over ``grid``; zeroes steps."""
+        grid = tuple(int(g) for g in grid)
+        if grid != self.grid:
+            self.grid = grid
+            self.order = initial_order.clone()
+            self.steps = torch.zeros(grid[0] * grid[1], dtype=torch.int32, device=initial_order.device)
+        else:
+            self.steps.zero_()
+        return self.order, self.steps
+
+    def update(self) -> None:
+        """Sort the tiles just measured (call after the launch, same stream)."""
+        if self.steps is not None:
+            idx = torch.argsort(self.steps, descending=True, stable=True)
+            self.order.copy_(idx.to(torch.int32))

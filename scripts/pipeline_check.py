@@ -46,8 +46,8 @@ def main():
     tf, cam, spec, settings = bench.scene_objects(cfg, "cone")
     dvol, _ = bench.device_volume_for(cfg, dev)
     out = {}
-    for world in (1, 8):
-        fr = FakeRank(dvol, tf, cam, spec, settings, device=dev, rank=0, world=world)
+    for world in (1, 2, 4, 8):
+        fr = FakeRank(dvol, tf, cam, spec, settings, device=dev, rank=0, world=world, feedback=world > 1)
         serial = timed(lambda: (fr.build(), fr.march(False)))
         ref = fr.chunk.clone()
         pipe = FramePipeline(fr)
@@ -56,7 +56,8 @@ def main():
             pipe.step()
             pipe.drain()  # (per-frame drain keeps the timing honest: every build counted)
         piped_drain = timed(step)
-        pipe2 = FramePipeline(FakeRank(dvol, tf, cam, spec, settings, device=dev, rank=0, world=world))
+        pipe2 = FramePipeline(FakeRank(dvol, tf, cam, spec, settings, device=dev, rank=0, world=world,
+                                       feedback=world > 1))
         piped = timed(lambda: pipe2.step())
         same = bool(torch.equal(pipe2.fr.chunk, ref))
         out[world] = {"serial_ms": serial, "pipelined_ms": piped, "pipelined_drain_each_ms": piped_drain,

@@ -19,6 +19,8 @@ def main():
     buf = sb.build_attenuation_buffer(dvol, tf, cam, spec)
     band = int(sys.argv[1]) if len(sys.argv) > 1 else 8
     hf = {"hf": True, "nohf": False}.get(sys.argv[2]) if len(sys.argv) > 2 else None  # None: library default
+    fb = len(sys.argv) > 3 and sys.argv[3] == "fb"  # measured (feedback) heavy-first order
+    from paper_2008_06134_b200.schedule import TileFeedback
     out = {}
     for world in (1, 2, 4, 8):
         br = band if band > 0 else -(-(settings.viewport[1] // world) // 8) * 8  # 0: contiguous blocks
@@ -29,9 +31,14 @@ def main():
         ranks = range(world)
         times = []
         for rank in ranks:  # every rank's share, one after the other
+            feed = TileFeedback() if fb else None
+            if fb:  # one frame to measure the tiles
+                sb.render_device(dvol, tf, settings, buf, rank=rank, world=world, band_rows=br, heavy_first=hf,
+                                 feedback=feed)
             e0.record()
             for _ in range(5):
-                sb.render_device(dvol, tf, settings, buf, rank=rank, world=world, band_rows=br, heavy_first=hf)
+                sb.render_device(dvol, tf, settings, buf, rank=rank, world=world, band_rows=br, heavy_first=hf,
+                                 feedback=feed)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 5)

@@ -527,3 +527,26 @@ def test_ray_groups_identical(sb, mode):
                     asm[py] = part[lr]
         assert torch.equal(asm, full), world
         assert total == int(n_full.item())
+
+
+def test_measured_tile_order_identical(sb):
+    """Heavy-first by measured tile costs (K2 writes each tile's longest-ray
+    sample count; the next frame dispatches in that order): same image, and
+    the measured order puts the costliest tile first."""
+    import torch
+    from paper_2008_06134_b200.datasets import make_sphere_blobs
+    from paper_2008_06134_b200.schedule import TileFeedback
+    v = make_sphere_blobs((48, 48, 48), seed=3)
+    tf = sb.preset("hot")
+    d = (0.3, -0.5, 0.8)
+    settings = sb.RenderSettings(camera=sb.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5)),
+                                 light=sb.Light(direction=d), viewport=(200, 120), step=1 / 128, shading_mode="cone")
+    buf = sb.build_attenuation_buffer(v, tf, sb.LightCamera.fit(d, (1, 1, 1), (64, 64)), sb.make_slice_stack(d, 32))
+    ref = sb.render_device(v, tf, settings, buf, heavy_first=False)
+    fb = TileFeedback()
+    for _ in range(3):
+        img = sb.render_device(v, tf, settings, buf, heavy_first=True, feedback=fb)
+        assert torch.equal(img, ref)
+    steps = fb.steps.cpu().numpy()
+    assert steps.max() > 0
+    assert steps[int(fb.order[0].item())] == steps.max()
