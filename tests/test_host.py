@@ -203,3 +203,23 @@ def test_skip_clear_hint():
     assert not device.skip_clear_hint(V, preset("hot").lut)   # no voxel reaches the run
     assert device.skip_clear_hint(V, tf.resolve(1 / 256))
     assert not device.skip_clear_hint(V, lut)
+
+
+def test_tile_feedback_order():
+    """schedule.TileFeedback: the measured order lists tiles by decreasing
+    longest-ray sample count (stable for ties), is kept across frames of
+    the same grid and reset when the grid changes (device-agnostic logic,
+    run here on CPU tensors)."""
+    import torch
+    from paper_2008_06134_b200.schedule import TileFeedback
+    fb = TileFeedback()
+    init = torch.arange(6, dtype=torch.int32)
+    order, steps = fb.prepare((3, 2, 16, 8), init)
+    assert torch.equal(order, init) and int(steps.sum()) == 0
+    steps.copy_(torch.tensor([5, 9, 0, 9, 2, 7], dtype=torch.int32))
+    fb.update()
+    assert fb.order.tolist() == [1, 3, 5, 0, 4, 2]
+    order2, steps2 = fb.prepare((3, 2, 16, 8), init)
+    assert order2 is fb.order and int(steps2.sum()) == 0          # same grid: order kept, costs zeroed
+    order3, _ = fb.prepare((2, 2, 32, 8), torch.arange(4, dtype=torch.int32))
+    assert order3.tolist() == [0, 1, 2, 3]                          # new grid: fresh initial order
