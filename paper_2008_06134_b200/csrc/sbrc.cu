@@ -13,8 +13,18 @@ namespace {
 // the cube, alpha = lut(trilinear(p)) and T *= 1 - alpha. Texels are
 // independent, so no grid-wide barrier or per-slice launch is needed. The
 // quad of layer k needs layer k+1, so it is emitted one slice late.
+// K1 block: 4 warps (light rows), compiled for 6 blocks/SM (80 registers,
+// 24 warps/SM, as with 8-warp blocks) — the finer blocks even out the last
+// wave of uneven texel rows (A/B in profiles/r01_notes.md: config 3 build
+// 0.466 -> 0.417 ms, config 2 0.209 -> 0.179, config 4 3.61 -> 3.47).
+#ifndef SBRC_BUILD_ROWS
+#define SBRC_BUILD_ROWS 4
+#endif
+#ifndef SBRC_BUILD_MINB
+#define SBRC_BUILD_MINB 6
+#endif
 template <int VT, bool UNIT>
-__global__ void __launch_bounds__(256) build_kernel(const sbrc_build_params P) {
+__global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_kernel(const sbrc_build_params P) {
   __shared__ double lut[SBRC_LUT_SIZE];
   __shared__ double u8tab[256];
   for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x * blockDim.y)
@@ -359,8 +369,8 @@ void has_passes(const sbrc_half_angle_params& p, int k0, int k1, cudaStream_t s)
 
 template <int VT>
 void launch_build(const sbrc_build_params& p, cudaStream_t s) {
-  dim3 block(32, 8);  // warps are rows of 31 owned texels (build_kernel)
-  dim3 grid((p.light.width + 30) / 31, (p.row_end - p.row_begin + 7) / 8);
+  dim3 block(32, SBRC_BUILD_ROWS);  // warps are rows of 31 owned texels (build_kernel)
+  dim3 grid((p.light.width + 30) / 31, (p.row_end - p.row_begin + SBRC_BUILD_ROWS - 1) / SBRC_BUILD_ROWS);
   if (unit_box(p.volume)) build_kernel<VT, true><<<grid, block, 0, s>>>(p);
   else build_kernel<VT, false><<<grid, block, 0, s>>>(p);
 }
