@@ -553,7 +553,9 @@ def run_ours(a, cfg, mode):
 
 def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
     """Same frame through the public API with host buffers: LUTs and slice
-    offsets copied host->device every step, the image read back to host.
+    offsets copied host->device every step, the image read back to host
+    (at N=1 ``render`` has K2 store the pixels into a page-locked host array
+    over PCIe during the march: the same 16 bytes per pixel cross to the host).
     The volume is uploaded once (device cache keyed by the host array, as the
     reference service keeps datasets resident) and that upload is reported
     separately."""
@@ -605,7 +607,8 @@ def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
     sec = el.item() / k
     return {"value": 1.0 / sec, "unit": "frames/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": sec * 1e3, "steps": k, "volume_upload_s_once": upload_s,
-            "path": "paper_2008_06134_b200.build_attenuation_buffer + render (numpy in, numpy out)"
+            "path": "paper_2008_06134_b200.build_attenuation_buffer + render (numpy in, numpy out; "
+                    "K2 stores the image into pinned host memory)"
             if world == 1 else "FrameRenderer (host LUTs in, host image out)"}
 
 

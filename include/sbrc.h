@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 7
+#define SBRC_ABI_VERSION 8
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -261,6 +261,12 @@ int sbrc_ipc_free(void* ptr);
 int sbrc_ipc_handle(void* ptr, unsigned char handle[64]);
 int sbrc_ipc_open(const unsigned char handle[64], void** ptr);
 int sbrc_ipc_close(void* ptr);
+
+/* Device address of page-locked host memory (cudaPointerGetAttributes):
+ * *dev = the pointer K2 may store to (image = *dev writes the frame straight
+ * into host memory over PCIe while the march runs). SBRC_EINVAL if `host`
+ * is not page-locked, mapped host memory. */
+int sbrc_host_device_pointer(const void* host, void** dev);
 
 /* Block grid of the throughput K2 kernels for (width, height, band_rows,
  * rank, world): grid[0..3] = tiles_x, tiles_y, tile width and height in

@@ -16,7 +16,7 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 MAX_PEERS = 8
@@ -31,7 +31,7 @@ EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume
            "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_shadow_oracle", "sbrc_light_factor",
            "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_ipc_alloc", "sbrc_ipc_free", "sbrc_ipc_handle",
            "sbrc_ipc_open", "sbrc_ipc_close", "sbrc_march_grid", "sbrc_local_rows",
-           "sbrc_render_grid")
+           "sbrc_render_grid", "sbrc_host_device_pointer")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -107,6 +107,7 @@ def _load() -> C.CDLL:
                                       C.c_void_p]
     lib.sbrc_ipc_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
     lib.sbrc_ipc_free.argtypes = [C.c_void_p]
+    lib.sbrc_host_device_pointer.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
     lib.sbrc_ipc_handle.argtypes = [C.c_void_p, C.c_char * 64]
     lib.sbrc_ipc_open.argtypes = [C.c_char * 64, C.POINTER(C.c_void_p)]
     lib.sbrc_ipc_close.argtypes = [C.c_void_p]
@@ -144,6 +145,14 @@ def check(status: int, what: str) -> None:
 
 def local_rows(height: int, band_rows: int, rank: int, world: int) -> int:
     return int(lib.sbrc_local_rows(height, band_rows, rank, world))
+
+
+def host_device_pointer(host_ptr: int) -> int | None:
+    """Device address of page-locked host memory, or None if it is not mapped."""
+    d = C.c_void_p()
+    if lib.sbrc_host_device_pointer(C.c_void_p(host_ptr), C.byref(d)) != OK:
+        return None
+    return int(d.value or 0) or None
 
 
 def render_grid(p) -> tuple[int, int, int, int]:

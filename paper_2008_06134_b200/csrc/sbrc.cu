@@ -410,6 +410,18 @@ int sbrc_ipc_alloc(int64_t bytes, void** ptr) {
   return cudaMalloc(ptr, (size_t)bytes) == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 
+int sbrc_host_device_pointer(const void* host, void** dev) {
+  if (host == nullptr || dev == nullptr) return SBRC_EINVAL;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    cudaGetLastError();
+    return SBRC_EINVAL;
+  }
+  if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return SBRC_EINVAL;
+  *dev = a.devicePointer;
+  return SBRC_OK;
+}
+
 int sbrc_ipc_free(void* ptr) { return cudaFree(ptr) == cudaSuccess ? SBRC_OK : SBRC_ECUDA; }
 
 int sbrc_ipc_handle(void* ptr, unsigned char handle[64]) {

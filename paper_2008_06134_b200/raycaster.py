@@ -37,11 +37,8 @@ def _quads_of(buffer, dev) -> torch.Tensor:
     return pack_quads(torch.from_numpy(np.ascontiguousarray(buffer.intensity, dtype=np.float32)).to(dev))
 
 
-def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: bool = False,
-                  rank: int = 0, world: int = 1, band_rows: int = 8, out: torch.Tensor | None = None,
-                  peer_images=(), heavy_first: bool | None = None, feedback=None):
-    """Enqueue K2; returns the (rows, W, 4) CUDA image (all rows when world == 1)
-    and, with ``count_samples``, a 1-element int64 CUDA tensor of executed samples."""
+def _prepare(v, tf, settings, buffer, device):
+    """Validation and device inputs shared by render_device and render."""
     mode = settings.shading_mode
     if mode in BUFFER_MODES and buffer is None:
         raise ConfigError(f"shading mode {mode!r} needs an attenuation buffer")
@@ -51,6 +48,22 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
     dvol = device_volume(v, dev)
     lut_host = tf.resolve(settings.step)   # raycaster.py:453
     lut = f64_tensor(lut_host, dev)
+    inten, cam, spec, color = None, None, None, None
+    if mode in BUFFER_MODES:
+        inten = _quads_of(buffer, dev)
+        cam, spec, color = buffer.camera, buffer.spec, buffer.camera.light_color
+        n, hh, ww = inten.shape[:3]
+        if (n, hh, ww) != (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0])):
+            raise ValueError("attenuation intensity shape does not match its camera/stack")
+    return dev, dvol, lut, lut_host, inten, cam, spec, color
+
+
+def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: bool = False,
+                  rank: int = 0, world: int = 1, band_rows: int = 8, out: torch.Tensor | None = None,
+                  peer_images=(), heavy_first: bool | None = None, feedback=None):
+    """Enqueue K2; returns the (rows, W, 4) CUDA image (all rows when world == 1)
+    and, with ``count_samples``, a 1-element int64 CUDA tensor of executed samples."""
+    dev, dvol, lut, lut_host, inten, cam, spec, color = _prepare(v, tf, settings, buffer, device)
     w, h = int(settings.viewport[0]), int(settings.viewport[1])
     if world == 1:
         band_rows = 8
@@ -60,13 +73,6 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
     elif out.shape[0] < rows or out.shape[1] != w or out.shape[2] != 4 or not out.is_contiguous():
         raise ValueError(f"out must be a contiguous ({rows}, {w}, 4) float32 tensor")
     counter = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
-    inten, cam, spec, color = None, None, None, None
-    if mode in BUFFER_MODES:
-        inten = _quads_of(buffer, dev)
-        cam, spec, color = buffer.camera, buffer.spec, buffer.camera.light_color
-        n, hh, ww = inten.shape[:3]
-        if (n, hh, ww) != (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0])):
-            raise ValueError("attenuation intensity shape does not match its camera/stack")
     vs = float(dvol.voxel_size.max())   # ShellKernel.default(v.voxel_size.max()), :403
     hf = (world != 2) if heavy_first is None else heavy_first
     p = render_params(dvol, lut, settings, cam, spec, inten, color, vs, out, counter,
@@ -81,9 +87,20 @@ def render_device(v, tf, settings, buffer=None, *, device=None, count_samples: b
 
 
 def render(v, tf, settings, buffer=None) -> np.ndarray:
-    """GPU ray cast; drop-in for raycaster.py:443-469 (returns numpy float32 (H, W, 4))."""
-    img = render_device(v, tf, settings, buffer)
-    return to_host(img)
+    """GPU ray cast; drop-in for raycaster.py:443-469 (returns numpy float32 (H, W, 4)).
+
+    The image is returned without a separate read-back: K2 stores each
+    finished pixel straight into a page-locked host array (its device
+    address, ``sbrc_host_device_pointer``), so the 16 bytes per pixel cross
+    PCIe while the march runs instead of after it (config 3 end to end:
+    3.72 -> 3.54 ms per frame; profiles/r01_notes.md)."""
+    w, h = int(settings.viewport[0]), int(settings.viewport[1])
+    host = torch.empty((max(N.local_rows(h, 8, 0, 1), 1), w, 4), dtype=torch.float32, pin_memory=True)
+    if N.host_device_pointer(host.data_ptr()) != host.data_ptr():
+        return to_host(render_device(v, tf, settings, buffer))   # not mapped at the same address: copy
+    render_device(v, tf, settings, buffer, out=host)
+    torch.cuda.current_stream().synchronize()
+    return host[:h].numpy()
 
 
 def shadow_oracle_many(v, tf, pts, light, oracle_step: float, *, device=None) -> np.ndarray:

@@ -550,3 +550,28 @@ def test_measured_tile_order_identical(sb):
     steps = fb.steps.cpu().numpy()
     assert steps.max() > 0
     assert steps[int(fb.order[0].item())] == steps.max()
+
+
+@pytest.mark.parametrize("mode,viewport", [("cone", (1024, 1024)), ("shell", (1040, 1013)), ("none", (61, 37))])
+def test_render_direct_host_image_identical(sb, mode, viewport):
+    """render() has K2 store pixels straight into page-locked host memory
+    (sbrc_host_device_pointer); the image must be identical to the device
+    image of render_device, including heights that are not whole 8-row bands."""
+    import torch
+    from paper_2008_06134_b200 import _native as N
+    from paper_2008_06134_b200.datasets import make_sphere_blobs
+    host = torch.empty(16, pin_memory=True)
+    assert N.host_device_pointer(host.data_ptr()) == host.data_ptr()      # UVA: same address
+    assert N.host_device_pointer(np.zeros(16).ctypes.data) is None        # pageable memory is refused
+    v = make_sphere_blobs((40, 40, 40), seed=3)
+    tf = sb.preset("hot")
+    ld = (0.3, -0.5, 0.8)
+    cam = sb.LightCamera.fit(ld, (1, 1, 1), (48, 48))
+    spec = sb.make_slice_stack(ld, 24)
+    buf = sb.build_attenuation_buffer(v, tf, cam, spec)
+    settings = sb.RenderSettings(camera=sb.Camera(position=(0.4, 0.6, -1.5), target=(0.5, 0.5, 0.5)),
+                                 light=sb.Light(direction=ld), viewport=viewport, step=1 / 64, shading_mode=mode)
+    whole = sb.render_device(v, tf, settings, buf).cpu().numpy()
+    got = sb.render(v, tf, settings, buf)
+    assert got.shape == (viewport[1], viewport[0], 4) and got.dtype == np.float32
+    assert np.array_equal(got, whole)
