@@ -79,6 +79,8 @@ def parse():
     ap.add_argument("--no-pipeline", action="store_true",
                     help="disable overlapping the next frame's build with this frame's march")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-frame", action="store_true",
+                    help="reference arm: skip the unextrapolated config-2 frame; ours: skip the config-2 GPU frame")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     return a
@@ -136,6 +138,35 @@ def device_volume_for(cfg, dev):
     kind = 2 if q else 0
     one = np.ones(3)
     return DeviceVolume(t, kind, (d, d, d), np.zeros(3), one), None
+
+
+VOLUME_TYPE = {"blobs": ("f32", 4), "block_u8": ("u8", 1), "blobs_u16": ("u16", 2)}
+
+
+def workload_config(a, cfg, mode, world):
+    """The ``config`` object of the JSON line: the workload only, identical in
+    both arms (implementation choices go to ``setup``)."""
+    vt, vb = VOLUME_TYPE[cfg["volume"]]
+    V, A = cfg["dims"] ** 3 * vb, 4 * cfg["n"] * cfg["res"] ** 2
+    return {"workload": f"config {a.config}: {cfg['name']}", "volume": f"{cfg['dims']}^3 {vt}",
+            "image": [cfg["image"], cfg["image"]], "n_slices": cfg["n"], "slice_res": [cfg["res"], cfg["res"]],
+            "step": cfg["step"], "shading_mode": mode, "parallelism": f"image-tiles x{world}",
+            "l2": "inputs larger than L2 (volume %d MiB, buffer %d MiB)" % (V >> 20, A >> 20)}
+
+
+def host_cpu():
+    """CPU model and the cores this process may use (the reference arm's host)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"model": model, "logical_cpus": os.cpu_count(), "usable_cores": cores}
 
 
 def algorithmic_bytes(cfg, voxel_bytes, world):
@@ -265,13 +296,25 @@ def cpu_sample_plan(cfg):
     return b_rows, p_rows
 
 
+_CPU_CTX: dict = {}
+
+
+def set_cpu_context(vol, tf, cam, spec, settings, intensity):
+    """State the CPU workers read (set before forking a pool). The buffer is a
+    plain object with the reference AttenuationBuffer's fields."""
+    from types import SimpleNamespace
+    _CPU_CTX.update(vol=vol, tf=tf, cam=cam, spec=spec, settings=settings,
+                    buffer=None if intensity is None else SimpleNamespace(camera=cam, spec=spec, compensation_n=0.0,
+                                                                          intensity=intensity))
+
+
 def _cpu_build_part(args):
     rows, = args
     from oracle import slicecast_oracle as O
     g = _CPU_CTX
     t = time.perf_counter()
-    O.build_intensity(g["vol"], g["tf"].lut, g["cam"], g["spec"], 0.0, rows=rows)
-    return time.perf_counter() - t
+    out = O.build_intensity(g["vol"], g["tf"].lut, g["cam"], g["spec"], 0.0, rows=rows)
+    return time.perf_counter() - t, out
 
 
 def _cpu_march_part(args):
@@ -279,51 +322,36 @@ def _cpu_march_part(args):
     from oracle import slicecast_oracle as O
     g = _CPU_CTX
     t = time.perf_counter()
-    _, n = O.render_image(g["vol"], g["tf"].lut, g["settings"], g["buffer"], rows=rows, cols=cols,
-                          return_samples=True)
-    return time.perf_counter() - t, n
-
-
-_CPU_CTX: dict = {}
-
-
-def set_cpu_context(vol, tf, cam, spec, settings, intensity):
-    """State the CPU workers read (set before forking a pool)."""
-    from paper_2008_06134_b200.lightbuffer import AttenuationBuffer
-    _CPU_CTX.update(vol=vol, tf=tf, cam=cam, spec=spec, settings=settings,
-                    buffer=AttenuationBuffer(cam, spec, 0.0, intensity) if intensity is not None else None)
+    img, n = O.render_image(g["vol"], g["tf"].lut, g["settings"], g["buffer"], rows=rows, cols=cols,
+                            return_samples=True)
+    return time.perf_counter() - t, n, img
 
 
 def cpu_frame_sample(cfg, workers=1, pool=None):
     """Time the oracle on the bounded sample of one frame; extrapolate to the
-    full frame. Returns (frame_seconds, detail)."""
+    full frame. Returns (frame_seconds, detail, (build_rows_out, march_pixels_out))."""
     b_rows, p_rows = cpu_sample_plan(cfg)
     t0 = time.perf_counter()
     if pool is None:
-        _cpu_build_part((b_rows,))
+        built = [_cpu_build_part((b_rows,))[1]]
     else:
-        list(pool.map(_cpu_build_part, [(c,) for c in np.array_split(b_rows, workers) if len(c)]))
+        built = [o for _, o in pool.map(_cpu_build_part, [(c,) for c in np.array_split(b_rows, workers) if len(c)])]
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
     if pool is None:
-        _, samples = _cpu_march_part((p_rows, p_rows))
+        parts = [_cpu_march_part((p_rows, p_rows))]
     else:
         parts = list(pool.map(_cpu_march_part, [(r, p_rows) for r in np.array_split(p_rows, workers) if len(r)]))
-        samples = sum(n for _, n in parts)
     t_march = time.perf_counter() - t0
+    samples = sum(n for _, n, _ in parts)
     full_build = t_build * cfg["res"] / len(b_rows)
     full_march = t_march * cfg["image"] ** 2 / (len(p_rows) ** 2)
     detail = dict(build_rows=int(len(b_rows)), march_pixels=int(len(p_rows) ** 2), march_samples=int(samples),
+                  build_fraction=len(b_rows) / cfg["res"], march_fraction=len(p_rows) ** 2 / cfg["image"] ** 2,
                   t_build_s=t_build, t_march_s=t_march, build_s_extrapolated=full_build,
-                  march_s_extrapolated=full_march)
-    return full_build + full_march, detail
-
-
-def _cpu_full_build_part(args):
-    rows, = args
-    from oracle import slicecast_oracle as O
-    g = _CPU_CTX
-    return O.build_intensity(g["vol"], g["tf"].lut, g["cam"], g["spec"], 0.0, rows=rows)
+                  march_s_extrapolated=full_march, extrapolated=True)
+    outputs = (np.concatenate(built, axis=1), np.concatenate([im for _, _, im in parts], axis=0))
+    return full_build + full_march, detail, outputs
 
 
 def cpu_sample_text(cfg):
@@ -334,42 +362,98 @@ def cpu_sample_text(cfg):
 
 
 # --------------------------------------------------------------- reference arm
+def oracle_scene(cfg, mode):
+    """The config's inputs built by the oracle's scene port (no product code)."""
+    from oracle import scenes as S
+    tf = S.preset(cfg["tf"])
+    cam = S.light_camera(LIGHT, (1.0, 1.0, 1.0), (cfg["res"], cfg["res"]))
+    spec = S.slice_stack(LIGHT, cfg["n"])
+    settings = S.render_settings(EYE, TARGET, (cfg["image"], cfg["image"]), cfg["step"], mode, LIGHT)
+    d = cfg["dims"]
+    if cfg["volume"] == "block_u8":
+        _, f = S.raw_roundtrip(S.perforated_block(d, cfg["seed"]), "u8")
+        vol = S.volume(f, scalar_type="u8")
+    elif cfg["volume"] == "blobs_u16":
+        _, f = S.raw_roundtrip(S.blob_field(d, cfg["seed"]), "u16")
+        vol = S.volume(f, scalar_type="u16")
+    else:
+        vol = S.volume(S.blob_field(d, cfg["seed"]))
+    return vol, tf, cam, spec, settings
+
+
+def _full_build(pool, workers, res):
+    parts = pool.map(_cpu_build_part, [(c,) for c in np.array_split(np.arange(res), workers) if len(c)])
+    return np.concatenate([o for _, o in parts], axis=1)
+
+
+def reference_full_frame(workers, ctx):
+    """One complete, unextrapolated config-2 frame of the reference CPU path
+    (build on all light rows, march on every pixel) on all host cores."""
+    cfg = CONFIGS[2]
+    vol, tf, cam, spec, settings = oracle_scene(cfg, cfg["mode"])
+    set_cpu_context(vol, tf, cam, spec, settings, None)
+    with ctx.Pool(workers) as pool:
+        t0 = time.perf_counter()
+        inten = _full_build(pool, workers, cfg["res"])
+        t_build = time.perf_counter() - t0
+        set_cpu_context(vol, tf, cam, spec, settings, inten)
+    with ctx.Pool(workers) as pool:  # forked after the stack exists
+        t0 = time.perf_counter()
+        rows = np.arange(cfg["image"])
+        parts = pool.map(_cpu_march_part, [(r, rows) for r in np.array_split(rows, workers) if len(r)])
+        t_march = time.perf_counter() - t0
+    frame = t_build + t_march
+    return {"config": f"config 2: {cfg['name']}", "fps": 1.0 / frame, "frame_s": frame, "build_s": t_build,
+            "march_s": t_march, "samples": int(sum(n for _, n, _ in parts)), "cores": workers,
+            "extrapolated": False}
+
+
 def run_reference(a, cfg, mode):
+    """The reference's CPU path (the oracle port: the reference is Python, so
+    nothing compiles into oracle/_ref) on all host cores, rank 0 only. Imports
+    nothing from the product package."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     import multiprocessing as mp
-    tf, cam, spec, settings = scene_objects(cfg, mode)
-    vol = host_volume(cfg)
-    workers = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    vol, tf, cam, spec, settings = oracle_scene(cfg, mode)
+    host = host_cpu()
+    workers = host["usable_cores"]
     ctx = mp.get_context("fork")
     inten = None
-    if mode != "none":  # the march reads the full stack: build it once, untimed, on all cores
+    if mode in ("sbrc_shadow", "shell", "cone"):  # the march reads the full stack: built once, untimed
         set_cpu_context(vol, tf, cam, spec, settings, None)
         with ctx.Pool(workers) as pool:
-            parts = pool.map(_cpu_full_build_part, [(c,) for c in np.array_split(np.arange(cfg["res"]), workers)
-                                                    if len(c)])
-        inten = np.concatenate(parts, axis=1)
+            inten = _full_build(pool, workers, cfg["res"])
     set_cpu_context(vol, tf, cam, spec, settings, inten)
     with ctx.Pool(workers) as pool:
         for _ in range(a.warmup):
             cpu_frame_sample(cfg, workers, pool)
-        times = []
+        times, walls = [], []
         detail = None
         for _ in range(a.steps):
-            ft, detail = cpu_frame_sample(cfg, workers, pool)
+            w0 = time.perf_counter()
+            ft, detail, _ = cpu_frame_sample(cfg, workers, pool)
+            walls.append(time.perf_counter() - w0)
             times.append(ft)
     frame_s = statistics.median(times)
     fps = 1.0 / frame_s
+    full = None if a.no_full_frame else reference_full_frame(workers, ctx)
     line = {
-        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": a.gpus,
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config {a.config}: {cfg['name']}", "shading_mode": mode,
-                   "parallelism": f"cpu processes x{workers}", "l2": "n/a (CPU)"},
+        "config": workload_config(a, cfg, mode, world),
+        "setup": {"cpu": host, "processes": workers, "path": "oracle/slicecast_oracle.py (numpy restatement "
+                  "of slicecast, bit-identical on the golden fixtures), fork pool over light rows / image rows"},
+        "extrapolated": True,
+        "sample_ms_per_step": statistics.median(walls) * 1e3,
         "gsamples_per_s": detail["march_samples"] / max(detail["t_march_s"], 1e-12) / 1e9,
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": "port",
-                         "sample": cpu_sample_text(cfg), "detail": detail},
+                         "sample": cpu_sample_text(cfg), "cpu_model": host["model"], "detail": detail},
+        "full_frame_config2": full,
+        "product_package_loaded": any(m.split(".")[0] == "paper_2008_06134_b200" for m in sys.modules),
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -460,7 +544,7 @@ def run_ours(a, cfg, mode):
         asm = [e[2].elapsed_time(e[3]) for e in evs]
     else:  # overlapped kernels: per-kernel times from a short serial run after the timed region
         ser = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(5)]
-        fr.quads, fr._render_params = pipe.bufs[0], None
+        fr.quads = pipe.bufs[0]
         for e in ser:
             e[0].record(stream)
             fr.build()
@@ -499,6 +583,10 @@ def run_ours(a, cfg, mode):
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["source"],
                 "algorithmic_bytes": d_bytes, "kernel_ms": d_ms,
                 "traffic": load_traffic(a.config, mode, dominant)}
+    roofline_k1 = {"bound": "hbm", "kernel": "build", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9,
+                   "peak": peaks["hbm_gbs"], "unit": "GB/s", "algorithmic_bytes": k1_bytes, "kernel_ms": k1_ms,
+                   "traffic": load_traffic(a.config, mode, "build")}
+    roofline_k1["frac"] = roofline_k1["achieved"] / peaks["hbm_gbs"]
     # Secondary view of K2: the bytes its gathers pull through L1/L2 per sample
     # (8 voxels + 2 16-byte texel quads per light lookup) against the SM-side
     # L1 data bandwidth (128 B/clk/SM at the max SM clock). The march is bound
@@ -510,26 +598,27 @@ def run_ours(a, cfg, mode):
           "unit": "GB/s", "bytes_per_sample": 8 * vbytes + 32 * lookups}
     l1["frac"] = l1["achieved"] / l1_peak
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        inten = fr.intensity.contiguous().cpu().numpy() if mode != "none" else None
-        cpu = cpu_baseline_leg(cfg, tf, cam, spec, settings, dvol, host_vol, inten)
+        inten = fr.intensity.contiguous().cpu().numpy() if mode in ("sbrc_shadow", "shell", "cone") else None
+        image = fr.assemble().cpu().numpy()
+        cpu, parity = cpu_baseline_leg(cfg, tf, cam, spec, settings, dvol, host_vol, inten, image)
+    full2 = None
+    if rank == 0 and world == 1 and not a.no_full_frame and a.config != 2:
+        full2 = gpu_full_frame_config2(dev)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
-            "config": {"workload": f"config {a.config}: {cfg['name']}", "volume": f"{cfg['dims']}^3 "
-                       + ("f32" if vbytes == 4 else ("u16" if vbytes == 2 else "u8")),
-                       "image": [cfg["image"], cfg["image"]], "n_slices": cfg["n"],
-                       "slice_res": [cfg["res"], cfg["res"]], "step": cfg["step"], "shading_mode": mode,
-                       "build": a.build if world > 1 else "single", "parallelism": f"image-tiles x{world}",
-                       "assemble": fr.assemble_mode if world > 1 else "none",
-                       "frame_pipelining": "build(f+1) overlaps march(f)" if pipelined else "off",
-                       "tile_order": "measured (previous frame)" if fr.feedback is not None else
-                       ("ray length" if (fr.world != 2 if fr.heavy_first is None else fr.heavy_first) else "natural"),
-                       "l2": "inputs larger than L2 (volume %d MiB, buffer %d MiB)" % (V >> 20, A >> 20)},
+            "config": workload_config(a, cfg, mode, world),
+            "setup": {"build": a.build if world > 1 else "single",
+                      "assemble": fr.assemble_mode if world > 1 else "none",
+                      "frame_pipelining": "build(f+1) overlaps march(f)" if pipelined else "off",
+                      "tile_order": "measured (previous frame)" if fr.feedback is not None else
+                      ("ray length" if (fr.world != 2 if fr.heavy_first is None else fr.heavy_first) else "natural"),
+                      "volume_in_hbm": "float32" if dvol.voxel_type == 0 else "raw"},
             "gsamples_per_s": samples / (k2_ms * 1e-3) / 1e9,
             "samples_per_frame": samples,
             "march_only_fps": 1000.0 / (k2_ms + asm_ms),
@@ -537,9 +626,12 @@ def run_ours(a, cfg, mode):
                         "build_gbs": k1_bytes / (k1_ms * 1e-3) / 1e9, "march_gbs": k2_bytes / (k2_ms * 1e-3) / 1e9,
                         "build_gtexel_slices_s": cfg["n"] * cfg["res"] ** 2 / (k1_ms * 1e-3) / 1e9},
             "roofline": roofline,
+            "roofline_build": roofline_k1,
             "roofline_l1": l1,
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "gpu_full_frame_config2": full2,
             "gpu_launches": 2 * a.steps,
             "clocks": clocks.summary(),
             "volume_gen_s": vol_gen_s,
@@ -612,18 +704,60 @@ def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
             if world == 1 else "FrameRenderer (host LUTs in, host image out)"}
 
 
-def cpu_baseline_leg(cfg, tf, cam, spec, settings, dvol, host_vol, intensity):
-    """The oracle port, single thread, on the bounded sample of this workload.
-    The march reads the GPU-built stack (bit-identical to the oracle's, see tests)."""
+def cpu_baseline_leg(cfg, tf, cam, spec, settings, dvol, host_vol, intensity, image):
+    """The oracle port, single thread, on the bounded sample of this workload,
+    and the parity of this run's GPU frame against it: the sampled light rows
+    of the stack (bit-exact expected) and the sampled pixels of the image
+    (north_star tolerance 1e-3; the tests assert 1e-4). The sampled march reads
+    the GPU-built stack, which the row check shows is the oracle's."""
     from paper_2008_06134_b200.scene import VolumeDataset
     if host_vol is None:
         raw = dvol.data.cpu().numpy()
         host_vol = VolumeDataset.from_array(raw) if dvol.voxel_type == 0 else \
             VolumeDataset.from_raw_array(raw.view(np.uint16) if dvol.voxel_type == 2 else raw)
     set_cpu_context(host_vol, tf, cam, spec, settings, intensity)
-    frame_s, detail = cpu_frame_sample(cfg)
-    return {"value": 1.0 / frame_s, "unit": "frames/s", "cores": 1, "kind": "port",
-            "sample": cpu_sample_text(cfg), "detail": detail}
+    frame_s, detail, (rows_cpu, pix_cpu) = cpu_frame_sample(cfg)
+    b_rows, p_rows = cpu_sample_plan(cfg)
+    parity = {"rows": int(len(b_rows)), "pixels": int(len(p_rows) ** 2), "tolerance": 1e-3}
+    if intensity is not None:
+        got = intensity[:, b_rows]
+        parity["build_rows_bit_exact"] = bool(np.array_equal(got, rows_cpu))
+        parity["build_max_abs"] = float(np.abs(got.astype(np.float64) - rows_cpu).max())
+    got = image[np.ix_(p_rows, p_rows)].astype(np.float64)
+    d = np.abs(got - pix_cpu.astype(np.float64))
+    mse = float(np.mean(d * d))
+    parity.update(max_abs=float(d.max()), psnr=float("inf") if mse == 0 else 10.0 * math.log10(1.0 / mse),
+                  over_1e_3=int((d > 1e-3).sum()), over_1e_4=int((d > 1e-4).sum()))
+    cpu = {"value": 1.0 / frame_s, "unit": "frames/s", "cores": 1, "kind": "port", "sample": cpu_sample_text(cfg),
+           "cpu_model": host_cpu()["model"], "detail": detail}
+    return cpu, parity
+
+
+def gpu_full_frame_config2(dev, frames: int = 20):
+    """Config 2 (256^3 u8 block -> 512^2, 128 slices, sbrc_shadow) on this GPU:
+    the same complete frame the reference arm times unextrapolated
+    (``full_frame_config2``), device-timed over ``frames`` frames."""
+    import torch
+    from paper_2008_06134_b200.frame import FrameRenderer
+    cfg = CONFIGS[2]
+    tf, cam, spec, settings = scene_objects(cfg, cfg["mode"])
+    dvol, _ = device_volume_for(cfg, dev)
+    fr = FrameRenderer(dvol.widened(), tf, cam, spec, settings, device=dev)
+    for _ in range(3):
+        fr.frame()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(frames):
+        fr.build()
+        fr.march(count_samples=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / frames
+    fr.close()
+    return {"config": f"config 2: {cfg['name']}", "fps": 1000.0 / ms, "ms_per_frame": ms, "frames": frames,
+            "timing": "CUDA events, build + march per frame, no pipelining"}
 
 
 def load_peaks():
@@ -660,9 +794,14 @@ def run_sweep(a, cfg, mode):
     tf, cam, spec, settings = scene_objects(cfg, mode)
     dvol, _ = device_volume_for(cfg, dev)
     fr = FrameRenderer(dvol, tf, cam, spec, settings, device=dev)
+    host_vol = None
+    if not a.no_cpu_baseline:
+        from paper_2008_06134_b200.scene import VolumeDataset
+        host_vol = VolumeDataset.from_array(dvol.data.cpu().numpy())
     stream = torch.cuda.current_stream()
     rows = []
     frames = cfg["frames"]
+    peak = load_peaks()["hbm_gbs"]
     for n in cfg["sweep_n"]:
         for res in cfg["sweep_res"]:
             lights = [orbit_light(360.0 * f / frames, 30.0) for f in range(frames)]
@@ -688,19 +827,52 @@ def run_sweep(a, cfg, mode):
             ms = start.elapsed_time(end) / frames
             b = sum(e[0].elapsed_time(e[1]) for e in ev) / frames
             m = sum(e[1].elapsed_time(e[2]) for e in ev) / frames
+            V = cfg["dims"] ** 3 * 4
+            A = 4 * n * res * res
+            I = 16 * cfg["image"] ** 2
             rows.append({"n_slices": n, "slice_res": res, "fps": 1000.0 / ms, "ms_per_frame": ms,
                          "build_ms": b, "march_ms": m,
-                         "build_gtexel_slices_s": n * res * res / (b * 1e-3) / 1e9})
+                         "build_gtexel_slices_s": n * res * res / (b * 1e-3) / 1e9,
+                         "roofline_build": {"algorithmic_bytes": V + A, "achieved_gbs": (V + A) / (b * 1e-3) / 1e9,
+                                            "frac": (V + A) / (b * 1e-3) / 1e9 / peak},
+                         "roofline_march": {"algorithmic_bytes": V + A + I,
+                                            "achieved_gbs": (V + A + I) / (m * 1e-3) / 1e9,
+                                            "frac": (V + A + I) / (m * 1e-3) / 1e9 / peak}})
+            if not a.no_cpu_baseline:
+                rows[-1]["parity"] = sweep_point_parity(cfg, fr, tf, host_vol)
             fr.set_light(cam, spec)  # release the large buffer before the next shape
             torch.cuda.empty_cache()
     head = next(r for r in rows if r["n_slices"] == 256 and r["slice_res"] == 512)
     line = {"metric": METRIC, "value": head["fps"], "unit": "frames/s", "n_gpus": 1, "steps": frames,
             "warmup": max(a.warmup, 3), "ms_per_step": head["ms_per_frame"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config 5: {cfg['name']}", "value_at": "n=256, res=512"},
+            "config": dict(workload_config(a, cfg, mode, 1), value_at="n=256, res=512"),
             "sweep": rows, "gpu_launches": 2 * frames * len(rows)}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def sweep_point_parity(cfg, fr, tf, host_vol, pixels: int = 8):
+    """Oracle check of the last frame of a sweep point (its orbit light): two
+    light rows of the stack (bit-exact expected) and, when the stack is small
+    enough to copy to the host, a pixels x pixels grid of the image."""
+    from oracle import slicecast_oracle as O
+    from types import SimpleNamespace
+    cam, spec = fr.cam, fr.spec
+    res = int(cam.resolution[1])
+    b_rows = np.array([res // 3, (2 * res) // 3])
+    want = O.build_intensity(host_vol, tf.lut, cam, spec, rows=b_rows)
+    got = fr.intensity[:, b_rows].contiguous().cpu().numpy()
+    out = {"build_rows": b_rows.tolist(), "build_rows_bit_exact": bool(np.array_equal(got, want))}
+    if int(spec.n_slices) * res * res <= (1 << 26):
+        img = fr.frame().cpu().numpy()
+        buf = SimpleNamespace(camera=cam, spec=spec, compensation_n=0.0,
+                              intensity=fr.intensity.contiguous().cpu().numpy())
+        pix = np.linspace(cfg["image"] // (2 * pixels), cfg["image"] - 1, pixels).astype(int)
+        want_img = O.render_image(host_vol, tf.lut, fr.settings, buf, rows=pix, cols=pix)
+        d = np.abs(img[np.ix_(pix, pix)].astype(np.float64) - want_img)
+        out.update(pixels=int(pixels * pixels), max_abs=float(d.max()), over_1e_3=int((d > 1e-3).sum()))
+    return out
 
 
 def main():

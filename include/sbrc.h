@@ -48,7 +48,7 @@ typedef enum sbrc_status {
   SBRC_EINVAL = -1,      /* bad parameter (ValueError in the reference)        */
   SBRC_ECONFIG = -2,     /* buffer mode without a buffer (ConfigError, raycaster.py:450) */
   SBRC_ECUDA = -3,       /* CUDA launch / runtime error                        */
-  SBRC_EUNSUPPORTED = -4 /* mode the hot path does not implement (phong, extinction) */
+  SBRC_EUNSUPPORTED = -4 /* shading mode outside SBRC_SHADE_NONE..SBRC_SHADE_EXTINCTION */
 } sbrc_status;
 
 typedef enum sbrc_voxel_type {
@@ -163,12 +163,14 @@ typedef struct sbrc_render_params {
   /* Optional dispatch order (heavy-first scheduling) over the rank-local
    * tiles of sbrc_render_grid, tile = ty * tiles_x + tx;
    * entry i is the tile dispatched i-th. NULL = natural order. n_tiles must
-   * equal the tile count (a stale table is ignored). */
+   * equal the tile count; a table sized for another grid is ignored, and so
+   * is tile_steps (natural order, no costs recorded). */
   int32_t n_tiles;
   const int32_t* tile_order;
   unsigned long long* sample_count;/* device counter (+= executed samples), may be NULL */
   /* Optional measured tile costs (n_tiles entries over the sbrc_render_grid
-   * tiles, zeroed by the caller): each block atomically maxes the executed
+   * tiles, zeroed by the caller; only written when n_tiles equals the
+   * launch's tile count, with or without tile_order): each block atomically maxes the executed
    * sample count of its longest ray into tile_steps[tile]. Sorted in
    * decreasing order it is the next frame's heavy-first tile_order. */
   unsigned int* tile_steps;

@@ -982,7 +982,13 @@ void launch_march_skip(const sbrc_render_params& p, cudaStream_t s) {
                         (SBRC_LATENCY_ALL && ((SH == SBRC_SHADE_SHELL && NS > 0) || SH == SBRC_SHADE_SHADOW)));
   const MarchShape m = march_shape(q, q.local_rows);
   const int n_tiles = m.tiles_x * m.tiles_y;
-  if (q.tile_order != nullptr && q.n_tiles != n_tiles) q.tile_order = nullptr;  // stale table
+  // A table sized for another grid is stale: dispatch in natural order and
+  // record no per-tile costs (tile_steps is indexed by this launch's grid and
+  // is only written when the caller sized it for exactly that grid).
+  if (q.n_tiles != n_tiles) {
+    q.tile_order = nullptr;
+    q.tile_steps = nullptr;
+  }
   constexpr int LG = SBRC_LAT_GROUP;
   const dim3 grid(m.tiles_x, m.tiles_y);
   if constexpr (LAT) {

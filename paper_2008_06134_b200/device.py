@@ -314,13 +314,19 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
         p.peer_images[i] = int(ptr)
     p.n_peers = len(peer_images)
     p.sample_count = counter.data_ptr() if counter is not None else None
+    # The struct holds raw device addresses: it keeps the tensors behind them
+    # alive for as long as a caller caches it (FrameRenderer, FramePipeline).
+    keep = [dvol.data, lut_dev, quads_dev, image, counter]
     if heavy_first:  # dispatch table over the exact grid sbrc_render will launch
         grid = N.render_grid(p)
         order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, grid)
         if feedback is not None:  # measured order of the previous frame (schedule.TileFeedback)
             order, steps = feedback.prepare(grid, order)
             p.tile_steps = steps.data_ptr()
+            keep.append(steps)
         p.tile_order, p.n_tiles = order.data_ptr(), int(order.numel())
+        keep.append(order)
+    p._keep = keep
     return p
 
 
@@ -337,6 +343,7 @@ def tile_order_for(settings, band_rows: int, rank: int, world: int, device, grid
            world, str(device), None if grid is None else tuple(grid))
     t = _ORDER_CACHE.get(key)
     if t is None:
+        # dropping the cache is safe: cached render params own their table (render_params._keep)
         if len(_ORDER_CACHE) > 64:
             _ORDER_CACHE.clear()
         t = torch.from_numpy(heavy_first(settings, band_rows, rank, world, grid)).to(device)

@@ -131,6 +131,8 @@ class FrameRenderer:
             feedback = self.world > 1 and heavy_first is not False
         self.feedback = TileFeedback() if feedback else None
         self.band_rows, self.comp = band_rows, compensation_n
+        # K2 params per (quads buffer, p2p raster parity); the structs own what they point to
+        self._params: dict = {}
         self.lut_host = tf.resolve(settings.step)
         self.lut = f64_tensor(self.lut_host, self.dev)
         self.counter = torch.zeros(1, dtype=torch.int64, device=self.dev)
@@ -148,33 +150,42 @@ class FrameRenderer:
         if assemble not in ("nccl", "p2p"):
             raise ValueError(f"assemble must be 'nccl' or 'p2p', got {assemble!r}")
         self.assemble_mode = "nccl"
-        self._peers: list[int] = []
+        self._peers: list[list[int]] = []
+        self._parity = 0  # p2p raster buffer of the next frame
         if assemble == "p2p" and self.world > 1:
             self._setup_p2p()
 
     # -------------------------------------------------------------- p2p
     def _setup_p2p(self) -> None:
+        """Map every rank's two raster images (double buffer, selected by frame
+        parity) into this process. Frame f's march stores into buffer f % 2 of
+        every rank; the barrier that ends frame f+1 orders frame f+2's stores
+        (the next writer of buffer f % 2) after every rank's reads of frame f
+        that were issued before it called frame f+1, so a slow consumer never
+        sees pixels of a later frame (the write-after-read race a single
+        raster would have)."""
         h, w = self.height, self.width
         try:
-            self._raster = _DeviceBuffer(h * w * 16)
-            mine = self._raster.handle()
+            self._rasters = [_DeviceBuffer(h * w * 16), _DeviceBuffer(h * w * 16)]
+            mine = b"".join(r.handle() for r in self._rasters)
         except RuntimeError:
-            self._raster, mine = None, b""
+            self._rasters, mine = [], b""
         handles = [None] * self.world
         dist.all_gather_object(handles, mine, group=self.group)
         if not all(handles):  # every rank sees the same list: consistent fallback
             self._fallback()
             return
-        raster = torch.as_tensor(self._raster, device=self.dev).view(h, w, 4)
-        peers, opened = [], []
+        rasters = [torch.as_tensor(r, device=self.dev).view(h, w, 4) for r in self._rasters]
+        peers, opened = [[], []], []
         try:
             for r, hd in enumerate(handles):
-                if r == self.rank:
-                    peers.append(self._raster.ptr)
-                else:
-                    ptr = open_peer(hd)
-                    opened.append(ptr)
-                    peers.append(ptr)
+                for b in range(2):
+                    if r == self.rank:
+                        peers[b].append(self._rasters[b].ptr)
+                    else:
+                        ptr = open_peer(hd[64 * b:64 * (b + 1)])
+                        opened.append(ptr)
+                        peers[b].append(ptr)
             ok = True
         except RuntimeError:
             ok = False
@@ -187,10 +198,10 @@ class FrameRenderer:
             return
         ref = self.frame().clone()  # NCCL path
         self._peers = peers
-        self._raster_t = raster
+        self._raster_t = rasters
         self.assemble_mode = "p2p"
-        self._render_params = None
-        same = bool(torch.equal(ref, self.frame()))
+        self._params.clear()
+        same = bool(torch.equal(ref, self.frame())) and bool(torch.equal(ref, self.frame()))  # both buffers
         if not self._all_ok(same):
             self._fallback()
 
@@ -203,7 +214,7 @@ class FrameRenderer:
     def _fallback(self) -> None:
         self._peers = []
         self.assemble_mode = "nccl"
-        self._render_params = None
+        self._params.clear()
 
     # -------------------------------------------------------------- light
     def prepare_light(self, light_cam, spec):
@@ -220,7 +231,7 @@ class FrameRenderer:
         if getattr(self, "_shape", None) != shape:
             self.set_light(cam, spec)
         self.cam, self.spec, self.alpha, self.offsets = cam, spec, alpha, offsets
-        self._render_params = None
+        self._params.clear()
 
     def set_light(self, light_cam, spec) -> None:
         """(Re)allocate the attenuation buffer for a light frame (config 5 moves the light)."""
@@ -242,7 +253,7 @@ class FrameRenderer:
             self.shard = torch.empty((hs, n, w, 4), dtype=torch.float32, device=self.dev)
             self.quads = self.storage[:h].permute(1, 0, 2, 3)  # (n, H, W, 4) view
         self.intensity = self.quads[..., 0]
-        self._render_params = None
+        self._params.clear()
 
     # -------------------------------------------------------------- stages
     def build(self) -> None:
@@ -256,22 +267,25 @@ class FrameRenderer:
         all_gather_into(self.storage, self.shard, self.group)
 
     def march(self, count_samples: bool = True) -> None:
-        if self._render_params is None:
+        p2p = self.assemble_mode == "p2p"
+        key = (self.quads.data_ptr(), self._parity if p2p else 0)
+        params = self._params.get(key)
+        if params is None:
             buf_modes = self.settings.shading_mode in ("sbrc_shadow", "shell", "cone")
-            p2p = self.assemble_mode == "p2p"
-            self._render_params = render_params(
+            params = render_params(
                 self.dvol, self.lut, self.settings, self.cam if buf_modes else None,
                 self.spec if buf_modes else None, self.quads if buf_modes else None,
                 self.cam.light_color, float(self.dvol.voxel_size.max()), None if p2p else self.chunk, self.counter,
                 band_rows=self.band_rows, rank=self.rank, world=self.world, voxel_size=self.dvol.voxel_size,
-                peer_images=self._peers if p2p else (),
+                peer_images=self._peers[key[1]] if p2p else (),
                 heavy_first=(self.feedback is not None or self.world != 2) if self.heavy_first is None
                 else self.heavy_first,
                 lut_host=self.lut_host, feedback=self.feedback)
+            self._params[key] = params
         elif self.feedback is not None and self.feedback.steps is not None:
             self.feedback.steps.zero_()
-        self._render_params.sample_count = self.counter.data_ptr() if count_samples else None
-        N.check(N.lib.sbrc_render(self._render_params, current_stream_handle()), "sbrc_render")
+        params.sample_count = self.counter.data_ptr() if count_samples else None
+        N.check(N.lib.sbrc_render(params, current_stream_handle()), "sbrc_render")
         if self.feedback is not None:
             self.feedback.update()
 
@@ -285,20 +299,31 @@ class FrameRenderer:
                 else:  # gloo (tests): host barrier after this rank's march completed
                     torch.cuda.current_stream(self.dev).synchronize()
                     dist.barrier(group=self.group)
-                return self._raster_t
+                out = self._raster_t[self._parity]
+                self._parity ^= 1
+                return out
             all_gather_into(self.gathered, self.chunk, self.group)
             torch.index_select(self.gathered, 0, self.perm, out=self.image)
         return self.image
 
     def close(self) -> None:
-        """Unmap peer images and free the IPC raster (p2p mode)."""
-        for ptr in getattr(self, "_opened", []):
+        """Unmap the peer rasters, then free this rank's own (p2p mode).
+        Collective: every rank first finishes its work and closes its
+        mappings, and only after a barrier frees the rasters others mapped."""
+        opened = getattr(self, "_opened", [])
+        rasters = getattr(self, "_rasters", [])
+        if not opened and not rasters:
+            return
+        torch.cuda.synchronize(self.dev)  # no march of this rank still stores to a peer
+        for ptr in opened:
             N.lib.sbrc_ipc_close(ptr)
         self._opened = []
-        if getattr(self, "_raster", None) is not None:
-            torch.cuda.synchronize(self.dev)
-            self._raster.free()
-            self._raster = None
+        if self.distributed and self.world > 1:
+            dist.barrier(group=self.group)  # every importer has closed its handles
+        for r in rasters:
+            r.free()
+        self._rasters = []
+        self._peers = []
 
     def frame(self) -> torch.Tensor:
         self.build()
@@ -330,7 +355,6 @@ class FramePipeline:
         self.build_stream = torch.cuda.Stream(fr.dev)
         self.built = [torch.cuda.Event(), torch.cuda.Event()]
         self.released = [torch.cuda.Event(), torch.cuda.Event()]
-        self.params = [None, None]
         self.f = 0
         self.pending = None  # buffer index whose build is in flight
 
@@ -349,13 +373,8 @@ class FramePipeline:
         self.pending = 1 - i
         main = torch.cuda.current_stream(fr.dev)
         main.wait_event(self.built[i])
-        if self.params[i] is None:
-            fr.quads, fr._render_params = self.bufs[i], None
-            fr.march(count_samples)
-            self.params[i] = fr._render_params
-        else:
-            fr._render_params = self.params[i]
-            fr.march(count_samples)
+        fr.quads = self.bufs[i]  # the renderer keeps one params struct per buffer
+        fr.march(count_samples)
         self.released[i].record(main)
         img = fr.assemble()
         self.f += 1

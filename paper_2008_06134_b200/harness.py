@@ -18,9 +18,11 @@ from __future__ import annotations
 import csv
 import hashlib
 import io
+import itertools
 import json
 import threading
 from collections import OrderedDict
+from concurrent.futures import Future
 from dataclasses import dataclass
 
 import numpy as np
@@ -57,58 +59,96 @@ def _buffer_bytes(buf) -> int:
     return 0 if q is None else q.numel() * q.element_size()
 
 
+class _Slot:
+    """One cache key: a future for the buffer, and the CUDA event recorded on
+    the building stream right after K1 was enqueued (None off-GPU)."""
+
+    __slots__ = ("future", "ready", "nbytes")
+
+    def __init__(self):
+        self.future: Future = Future()
+        self.ready = None
+        self.nbytes = 0
+
+
 class BufferCache:
-    """Bounded LRU of device-resident attenuation buffers with atomic get-or-build."""
+    """LRU of HBM-resident attenuation buffers, bounded by entry count and bytes.
+
+    Same contract as the service's cache (service.py:98-130): ``get_or_build``
+    returns ``(buffer, hit)`` and concurrent requests for one key build once.
+    The mechanism is device-aware: a key maps to a slot holding a future.
+    The first requester becomes the builder — it enqueues K1 on its stream
+    and records a CUDA event after it, then resolves the future without
+    waiting for the GPU. Every other requester (another thread, or a later
+    call) takes the buffer from the future and makes *its* current stream
+    wait on that event, so readiness is ordered on the device and no host
+    thread blocks on a build that is merely in flight. A builder that raises
+    resolves the future with the exception: concurrent waiters re-raise it,
+    and the slot is dropped so the next request builds again. In-flight
+    slots are never evicted."""
 
     def __init__(self, max_entries: int = 8, max_bytes: int | None = None):
         self.max_entries = max_entries
         self.max_bytes = max_bytes
-        self._entries: OrderedDict = OrderedDict()
-        self._pending: dict = {}
+        self._slots: OrderedDict = OrderedDict()
         self._lock = threading.Lock()
 
     def __len__(self) -> int:
-        return len(self._entries)
+        with self._lock:
+            return sum(1 for s in self._slots.values() if s.future.done() and s.future.exception() is None)
 
     @property
     def bytes(self) -> int:
-        return sum(_buffer_bytes(v) for v in self._entries.values())
+        with self._lock:
+            return sum(s.nbytes for s in self._slots.values())
 
     def get_or_build(self, key, builder):
-        """(value, hit). Concurrent requests for one key build once; a failed
-        build releases the waiters (service.py:107-130)."""
-        while True:
-            with self._lock:
-                if key in self._entries:
-                    self._entries.move_to_end(key)
-                    return self._entries[key], True
-                event = self._pending.get(key)
-                if event is None:
-                    self._pending[key] = threading.Event()
-                    break
-            event.wait()
+        with self._lock:
+            slot = self._slots.get(key)
+            mine = slot is None
+            if mine:
+                slot = self._slots[key] = _Slot()
+            else:
+                self._slots.move_to_end(key)
+        if not mine:
+            value = slot.future.result()  # the builder's exception propagates to waiters
+            if slot.ready is not None:
+                torch.cuda.current_stream().wait_event(slot.ready)
+            return value, True
         try:
             value = builder()
-        except BaseException:
+        except BaseException as exc:
             with self._lock:
-                self._pending.pop(key).set()
+                if self._slots.get(key) is slot:
+                    del self._slots[key]
+            slot.future.set_exception(exc)
             raise
+        if torch.cuda.is_available() and getattr(value, "quads", None) is not None:
+            slot.ready = torch.cuda.Event()
+            slot.ready.record(torch.cuda.current_stream(value.quads.device))
+        slot.nbytes = _buffer_bytes(value)
+        slot.future.set_result(value)
         with self._lock:
-            self._entries[key] = value
-            self._evict()
-            self._pending.pop(key).set()
+            self._shrink()
         return value, False
 
-    def _evict(self) -> None:
-        while len(self._entries) > self.max_entries:
-            self._entries.popitem(last=False)
-        if self.max_bytes is not None:
-            while len(self._entries) > 1 and self.bytes > self.max_bytes:
-                self._entries.popitem(last=False)
+    def _shrink(self) -> None:
+        """Drop least-recently used finished slots until both bounds hold
+        (the newest entry always stays)."""
+        def over():
+            n = len(self._slots)
+            return n > self.max_entries or (self.max_bytes is not None and n > 1 and
+                                            sum(s.nbytes for s in self._slots.values()) > self.max_bytes)
+        for key in list(self._slots):
+            if not over():
+                break
+            if self._slots[key].future.done() and key != next(reversed(self._slots)):
+                del self._slots[key]
 
     def clear(self) -> None:
         with self._lock:
-            self._entries.clear()
+            for key in [k for k, s in self._slots.items() if s.future.done()]:
+                del self._slots[key]
 
 
 def cached_build(cache: BufferCache, dataset_id, v, tf, light, n_slices: int, resolution,
@@ -125,9 +165,39 @@ def cached_build(cache: BufferCache, dataset_id, v, tf, light, n_slices: int, re
 
 
 # ------------------------------------------------------------------ bench sweep
+def _res_text(r) -> str:
+    return f"{int(r[0])}x{int(r[1])}"
+
+
+def _res_parse(text: str) -> tuple:
+    w, h = text.split("x")
+    return int(w), int(h)
+
+
+def _ms(x) -> str:
+    return f"{float(x):.3f}"
+
+
+#: The reference's CSV schema (bench.py:26-36) as (column, render, parse):
+#: timings with three decimals, the resolution as "WxH", the step as repr.
+_SCHEMA = (
+    ("method", str, str),
+    ("n_slices", int, int),
+    ("buffer_resolution", _res_text, _res_parse),
+    ("sample_step", repr, float),
+    ("build_ms", _ms, float),
+    ("render_ms", _ms, float),
+    ("total_ms", _ms, None),  # derived: build + render
+    ("pass_count", int, int),
+    ("image_sha256", str, str),
+)
+assert tuple(c for c, _, _ in _SCHEMA) == CSV_FIELDS
+
+
 @dataclass
 class BenchRecord:
-    """One CSV row (bench.py:39-69)."""
+    """One sweep point; ``total_ms`` is derived. Negative timings are a
+    ValueError, as in the reference's record (bench.py:49-51)."""
 
     method: str
     n_slices: int
@@ -139,7 +209,7 @@ class BenchRecord:
     image_sha256: str = ""
 
     def __post_init__(self):
-        if self.build_ms < 0 or self.render_ms < 0:
+        if min(self.build_ms, self.render_ms) < 0:
             raise ValueError("timings must be >= 0")
 
     @property
@@ -147,19 +217,12 @@ class BenchRecord:
         return self.build_ms + self.render_ms
 
     def as_row(self) -> dict:
-        return {"method": self.method, "n_slices": self.n_slices,
-                "buffer_resolution": f"{self.buffer_resolution[0]}x{self.buffer_resolution[1]}",
-                "sample_step": repr(self.sample_step), "build_ms": f"{self.build_ms:.3f}",
-                "render_ms": f"{self.render_ms:.3f}", "total_ms": f"{self.total_ms:.3f}",
-                "pass_count": self.pass_count, "image_sha256": self.image_sha256}
+        return {col: out(getattr(self, col)) for col, out, _ in _SCHEMA}
 
 
 def parse_row(row: dict) -> BenchRecord:
-    w, h = row["buffer_resolution"].split("x")
-    return BenchRecord(method=row["method"], n_slices=int(row["n_slices"]), buffer_resolution=(int(w), int(h)),
-                       sample_step=float(row["sample_step"]), build_ms=float(row["build_ms"]),
-                       render_ms=float(row["render_ms"]), pass_count=int(row["pass_count"]),
-                       image_sha256=row["image_sha256"])
+    """Inverse of ``BenchRecord.as_row`` (the CSV round trip)."""
+    return BenchRecord(**{col: parse(row[col]) for col, _, parse in _SCHEMA if parse is not None})
 
 
 def image_sha256(img) -> str:
@@ -207,28 +270,23 @@ def render_scene(v, tf, settings, method: str, n_slices: int, resolution, compen
     return img, build_ms, e1.elapsed_time(e2), 1
 
 
+def _measure_point(v, tf, settings, method: str, n: int, res: tuple, repeats: int) -> BenchRecord:
+    """One sweep point: the first run only provides the image hash (warm-up),
+    the next ``repeats`` runs are averaged."""
+    runs = [render_scene(v, tf, settings, method, n, res) for _ in range(repeats + 1)]
+    timed = np.array([(b, r) for _, b, r, _ in runs[1:]], dtype=np.float64)
+    return BenchRecord(method=method, n_slices=n, buffer_resolution=res, sample_step=settings.step,
+                       build_ms=float(timed[:, 0].mean()), render_ms=float(timed[:, 1].mean()),
+                       pass_count=runs[-1][3], image_sha256=image_sha256(runs[0][0]))
+
+
 def run_sweep(v, tf, settings, methods, slices, resolutions, repeats: int = 3) -> list[BenchRecord]:
-    """Every (method, n_slices, resolution); mean of ``repeats`` timed runs after a
-    discarded warm-up whose image is hashed (bench.py:116-146)."""
+    """The reference sweep (bench.py:116-146) with device timing: every
+    (method, n_slices, resolution) in that nesting order."""
     if repeats < 1:
         raise ValueError("repeats must be >= 1")
-    out = []
-    for method in methods:
-        for n in slices:
-            for res in resolutions:
-                res = (res, res) if isinstance(res, int) else tuple(res)
-                builds, renders, digest = [], [], ""
-                for i in range(repeats + 1):
-                    img, b, r, passes = render_scene(v, tf, settings, method, n, res)
-                    if i == 0:
-                        digest = image_sha256(img)
-                        continue
-                    builds.append(b)
-                    renders.append(r)
-                out.append(BenchRecord(method=method, n_slices=n, buffer_resolution=res,
-                                       sample_step=settings.step, build_ms=float(np.mean(builds)),
-                                       render_ms=float(np.mean(renders)), pass_count=passes, image_sha256=digest))
-    return out
+    grid = itertools.product(methods, slices, [(r, r) if isinstance(r, int) else tuple(r) for r in resolutions])
+    return [_measure_point(v, tf, settings, m, n, res, repeats) for m, n, res in grid]
 
 
 def write_csv(records, fh_or_path) -> None:

@@ -287,12 +287,14 @@ def camera_frame(cam, viewport) -> dict:
         forward = normalize(cam.target - cam.position)
         right = normalize(np.cross(forward, cam.up))
         up2 = np.cross(right, forward)
+        for arr in (forward, right, up2):  # shared by every caller of this view: read-only
+            arr.setflags(write=False)
         fr = dict(forward=forward, right=right, up2=up2,
                   tan_half=math.tan(math.radians(cam.fov_deg) / 2.0), aspect=w / h)
         if len(_FRAME_CACHE) > 256:
             _FRAME_CACHE.clear()
         _FRAME_CACHE[key] = fr
-    return fr
+    return dict(fr)
 
 
 @dataclass(frozen=True)

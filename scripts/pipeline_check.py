@@ -20,7 +20,7 @@ class FakeRank(FrameRenderer):
         from paper_2008_06134_b200.frame import band_layout
         self.rows_local, _ = band_layout(self.height, self.band_rows, world)
         self.chunk = torch.zeros((self.rows_local, self.width, 4), dtype=torch.float32, device=self.dev)
-        self._render_params = None
+        self._params.clear()
 
     def assemble(self):
         return self.chunk

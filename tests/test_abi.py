@@ -83,3 +83,15 @@ def test_local_rows():
                 rows = [N.local_rows(h, br, r, world) for r in range(world)]
                 assert max(rows) == per_rank
                 assert sum(rows) >= h and sum(rows) - h < br * world
+
+
+def test_integration_doc_matches_header():
+    """INTEGRATION.md's binding snippet quotes the current ABI version and
+    names every exported entry point (the docs must not drift from the header)."""
+    text = open(os.path.join(ROOT, "include", "sbrc.h")).read()
+    version = int(re.search(r"#define SBRC_ABI_VERSION (\d+)", text).group(1))
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    quoted = [int(v) for v in re.findall(r"sbrc_abi_version\(\) == (\d+)", doc)]
+    assert quoted and all(v == version for v in quoted), (quoted, version)
+    for name in header_functions():
+        assert name in doc, f"{name} is not documented in INTEGRATION.md"

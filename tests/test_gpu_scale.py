@@ -100,8 +100,9 @@ def test_config3_full_size(sb):
     import bench
     cfg, tf, cam, spec, settings = _scene(3)
     v = bench.host_volume(cfg)  # 512^3 float32 blobs (numpy, bit-identical to the reference generator)
-    _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows=np.array([3, 200, 256, 511]),
-                      pix=np.arange(7, 1024, 64))
+    # the survey's stratified grid: every 16th light row, every 16th pixel row/column
+    _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows=np.arange(8, 512, 16),
+                      pix=np.arange(8, 1024, 16))
 
 
 def test_config3_transparent_buffer_equals_none(sb):
@@ -132,5 +133,5 @@ def test_config4_full_size(sb):
     raw = dvol.data.cpu().numpy().view(np.uint16)
     v = VolumeDataset.from_raw_array(raw)
     del raw
-    _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows=np.array([0, 511, 1023]),
-                      pix=np.arange(11, 2048, 256), gpu_vol=dvol)
+    _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows=np.arange(8, 1024, 16),
+                      pix=np.arange(8, 2048, 16), gpu_vol=dvol)

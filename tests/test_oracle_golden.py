@@ -158,3 +158,47 @@ def test_half_angle_oracle(tag):
     img, passes = O.half_angle(v, tf.lut, s, m["n"], tuple(m["light_res"]))
     assert passes == c["passes"] == 2 * m["n"]
     np.testing.assert_allclose(img, g[f"image_{tag}"], rtol=0, atol=1e-6)
+
+
+# ------------------------------------------------------------ config 5 (moving light) and the scene port
+def test_scene_port_matches_reference_objects(prim):
+    """oracle/scenes.py (used by bench.py's reference arm instead of the product
+    package) reproduces the reference's LUT, light frame and slice stack."""
+    from oracle import scenes as S
+    from paper_2008_06134_b200 import scene
+    for name in S.PRESETS:
+        assert np.array_equal(S.preset(name).lut, scene.preset(name).lut)
+    g = load_golden("config1")
+    assert __import__("hashlib").sha256(S.blob_field(64, 7).tobytes()).hexdigest() == str(g["volume_sha256"])
+    m = g["meta"]
+    cam = S.light_camera(m["light_dir"], m["light_color"], tuple(m["res"]))
+    spec = S.slice_stack(m["light_dir"], m["n"])
+    v = S.volume(S.blob_field(64, 7))
+    inten = O.build_intensity(v, S.preset(m["tf"]).lut, cam, spec)
+    assert np.array_equal(inten, g["intensity"])
+    blk = load_golden("block48_u8")
+    raw, f = S.raw_roundtrip(S.perforated_block(48, 3), "u8")
+    assert np.array_equal(f, blk["volume"])
+
+
+def test_orbit_light_cases_bit_exact():
+    """BASELINE config 5's orbit lights (orbit.ts:28-35): the oracle's build and
+    cone render equal the reference's at three azimuths."""
+    from oracle import scenes as S
+    g = load_golden("orbit32")
+    m = g["meta"]
+    v = S.volume(g["volume"])
+    tf = S.preset(m["tf"])
+    for az in m["azimuths"]:
+        ld = S.orbit_light(az, m["elevation"])
+        assert np.array_equal(np.asarray(ld), g[f"light_{int(az)}"])
+        cam = S.light_camera(ld, (1, 1, 1), tuple(m["res"]))
+        spec = S.slice_stack(ld, m["n"])
+        inten = O.build_intensity(v, tf.lut, cam, spec)
+        assert np.array_equal(inten, g[f"intensity_{int(az)}"])
+        st = S.render_settings(m["cam_pos"], m["cam_target"], m["viewport"], m["step"], "cone", ld,
+                               fov_deg=m["fov"])
+        from types import SimpleNamespace
+        buf = SimpleNamespace(intensity=inten, camera=cam, spec=spec)
+        img = O.render_image(v, tf.lut, st, buf)
+        assert np.array_equal(img, g[f"image_{int(az)}"])
