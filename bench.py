@@ -179,10 +179,13 @@ def algorithmic_bytes(cfg, voxel_bytes, world):
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
-    """SM clock, power and throttle reasons sampled during the timed region:
-    NVML polled every ~2 ms from a thread (so even a 50 ms region gets tens of
-    samples), nvidia-smi -lms 50 as the fallback. ``mark()`` brackets the
-    timed region and only samples inside it are summarised."""
+    """SM clock, power and throttle reasons sampled during the timed region.
+
+    Two samplers run side by side: NVML polled every ~2 ms from a thread
+    (tens of samples even in a 50 ms region) and ``nvidia-smi -lms 50`` as a
+    backup; the summary uses NVML rows when it got any, else the nvidia-smi
+    rows. ``mark()`` brackets the timed region and only samples inside it
+    (or the nearest one after its start) are summarised."""
 
     Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -195,44 +198,50 @@ class ClockSampler:
         self.thread = None
         self.rows = []
         self.t0 = self.t1 = None
-        self.source = None
+        self.errors = []
 
     def _nvml_loop(self, nv, h, bits):
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception as exc:  # noqa: BLE001
+            self.errors.append(f"nvml max clock: {exc!r}")
+            return
+        reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
         while not self.stop.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                rs = reasons(h)
                 self.rows.append((time.time(), float(sm), float(mx), pw,
                                   [nm for nm, b in zip(self.NAMES, bits) if rs & b]))
-            except Exception:  # noqa: BLE001 - a failed poll is just a missing sample
-                pass
+            except Exception as exc:  # noqa: BLE001 - a failed poll is just a missing sample
+                if len(self.errors) < 3:
+                    self.errors.append(f"nvml poll: {exc!r}")
             self.stop.wait(0.002)
 
     def __enter__(self):
+        import threading
+        self.stop = threading.Event()
         try:
-            import threading
             import pynvml as nv
             nv.nvmlInit()
             h = nv.nvmlDeviceGetHandleByIndex(int(self.index))
-            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
-            self.stop = threading.Event()
+            bits = tuple(getattr(nv, a, b) for a, b in (
+                ("nvmlClocksEventReasonHwSlowdown", 0x8), ("nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                ("nvmlClocksEventReasonSwThermalSlowdown", 0x20), ("nvmlClocksEventReasonSwPowerCap", 0x4)))
             self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h, bits), daemon=True)
             self.thread.start()
-            self.source = "nvml"
-            time.sleep(0.05)
-            return self
-        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
+        except Exception as exc:  # noqa: BLE001 - the nvidia-smi sampler still runs
+            self.errors.append(f"nvml init: {exc!r}")
             self.thread = None
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
-            self.source = "nvidia-smi"
-        except OSError:
+        except OSError as exc:
+            self.errors.append(f"nvidia-smi: {exc!r}")
             self.proc = None
         time.sleep(0.4)
         return self
@@ -241,16 +250,18 @@ class ClockSampler:
         setattr(self, which, time.time())
 
     def __exit__(self, *exc):
+        time.sleep(0.12)  # one more nvidia-smi period after the region
         if self.thread is not None:
             self.stop.set()
             self.thread.join(timeout=5)
         if self.proc is not None:
-            time.sleep(0.1)
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
     def _smi_rows(self):
         import datetime as _dt
+        if self.proc is None:
+            return []
         self.f.flush()
         self.f.seek(0)
         rows = []
@@ -267,14 +278,11 @@ class ClockSampler:
         return rows
 
     def summary(self):
-        if self.thread is not None:
-            rows = list(self.rows)
-        elif self.proc is not None:
-            rows = self._smi_rows()
-        else:
-            return None
+        rows, source = list(self.rows), "nvml"
         if not rows:
-            return None
+            rows, source = self._smi_rows(), "nvidia-smi"
+        if not rows:
+            return {"sm_mhz": None, "reasons": None, "samples": 0, "errors": self.errors}
         inside = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
         if not inside:  # timed region shorter than the sampling period: nearest sample after start
             after = [r for r in rows if self.t0 is None or r[0] >= self.t0]
@@ -282,7 +290,8 @@ class ClockSampler:
         reasons = sorted({nm for r in inside for nm in r[4]})
         return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": inside[0][2],
                 "power_w_max": max(r[3] for r in inside), "reasons": reasons, "samples": len(inside),
-                "window_s": (self.t1 - self.t0) if (self.t0 and self.t1) else None, "source": self.source}
+                "window_s": (self.t1 - self.t0) if (self.t0 and self.t1) else None, "source": source,
+                **({"errors": self.errors} if self.errors else {})}
 
 
 # --------------------------------------------------------------- CPU sample

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 8
+#define SBRC_ABI_VERSION 9
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -112,6 +112,18 @@ typedef struct sbrc_build_params {
   float* quads;
   int64_t quad_layer_stride;  /* in float4 units; (n, H, W) layout: H*W, [H][n][W]: W   */
   int64_t quad_row_stride;    /* in float4 units; (n, H, W) layout: W,   [H][n][W]: n*W */
+  /* Sparse output. write_sparse = 0: every quad is written. 1: for each
+   * texel only the quads of layers a march can read are written — the
+   * layers whose slice plane meets the cube inflated by write_reach along
+   * the texel's line (world units: the lateral reach of the consumer's
+   * lookups plus the bilinear footprint), widened by write_below layers
+   * toward the light and write_above away from it (plus two layers of
+   * rounding margin each side). Values written are identical to a full
+   * build; the other quads are left untouched. */
+  double write_reach;
+  int32_t write_below, write_above;
+  int32_t write_sparse;
+  int32_t reserved;
 } sbrc_build_params;
 
 typedef struct sbrc_render_params {

@@ -16,7 +16,7 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
-ABI_VERSION = 8
+ABI_VERSION = 9
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 MAX_PEERS = 8
@@ -52,7 +52,9 @@ class SbrcLightFrame(C.Structure):
 class SbrcBuildParams(C.Structure):
     _fields_ = [("volume", SbrcVolume), ("light", SbrcLightFrame), ("alpha_lut", C.c_void_p),
                 ("compensation_n", C.c_double), ("row_begin", C.c_int32), ("row_end", C.c_int32),
-                ("quads", C.c_void_p), ("quad_layer_stride", C.c_int64), ("quad_row_stride", C.c_int64)]
+                ("quads", C.c_void_p), ("quad_layer_stride", C.c_int64), ("quad_row_stride", C.c_int64),
+                ("write_reach", C.c_double), ("write_below", C.c_int32), ("write_above", C.c_int32),
+                ("write_sparse", C.c_int32), ("reserved", C.c_int32)]
 
 
 class SbrcRenderParams(C.Structure):

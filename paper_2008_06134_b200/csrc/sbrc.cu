@@ -59,14 +59,6 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
   const float* tab = reinterpret_cast<const float*>(u8tab);
   double T = 1.0;
   float prev = 0.0f;
-  auto emit = [&](float4* layer_row, float a, float b) {
-    float ra = __shfl_down_sync(0xffffffffu, a, 1), rb = __shfl_down_sync(0xffffffffu, b, 1);
-    if (x == L.width - 1) {
-      ra = a;
-      rb = b;
-    }
-    if (owner) layer_row[x] = make_float4(a, b, ra, rb);
-  };
   // One slice of the recurrence: stored = T (:169); if covered, alpha from the
   // cell, optional compensation (:193-196), T *= 1 - alpha (:197-198).
   auto step_slice = [&](bool covered, const Cell<VT>& cl) -> float {
@@ -86,12 +78,92 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
     py = dadd(base[1], dmul(off, L.light_dir[1]));
     pz = dadd(base[2], dmul(off, L.light_dir[2]));
   };
-  int k = 0;
+  // Slices whose texel-slice point is provably outside the cube need no
+  // float64 test: along the texel's line p(o) = base + o*L the cube is the
+  // offset interval [o_lo, o_hi] (slab test per axis); slices more than two
+  // slice spacings outside it are uncovered with a margin of >= 1.5 spacings
+  // times |L_c| >= 1e-6 (far above float64 rounding), so they store T
+  // unchanged. The warp runs the exact per-slice test over the union of its
+  // lanes' conservative ranges [kA, kB] and only stores before and after it
+  // (results bit-identical; near-axis-parallel light falls back to testing
+  // every slice).
+  const int n = L.n_slices;
+  int k_lo = 0, k_hi = n - 1;
+  {
+    const double spacing = (L.d_max - L.d_min) / n;
+    double olo = -INFINITY, ohi = INFINITY;
+    bool ranged = true;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double lc = L.light_dir[c];
+      if (fabs(lc) < 1e-6) {
+        ranged = false;
+      } else {
+        const double a = (0.0 - base[c]) / lc, b = (1.0 - base[c]) / lc;
+        olo = fmax(olo, fmin(a, b));
+        ohi = fmin(ohi, fmax(a, b));
+      }
+    }
+    if (ranged) {
+      const double kf = fmin(fmax((olo - L.d_min) / spacing - 0.5, -8.0), n + 8.0);
+      const double kl = fmin(fmax((ohi - L.d_min) / spacing - 0.5, -8.0), n + 8.0);
+      k_lo = max(0, (int)floor(kf) - 2);
+      k_hi = min(n - 1, (int)ceil(kl) + 2);
+    }
+  }
+  // Written layers [w_lo, w_hi] of this texel (all of them unless sparse):
+  // the slab test of the texel's line against the cube inflated by
+  // write_reach, widened by write_below / write_above plus two layers.
+  int w_lo = 0, w_hi = n - 1;
+  if (P.write_sparse) {
+    const double R = P.write_reach, spacing = (L.d_max - L.d_min) / n;
+    double olo = -INFINITY, ohi = INFINITY;
+    bool empty = false;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double lc = L.light_dir[c];
+      if (fabs(lc) < 1e-6) {  // nearly parallel: the coordinate moves < 1e-5 over the stack
+        if (base[c] < -R - 1e-5 || base[c] > 1.0 + R + 1e-5) empty = true;
+      } else {
+        const double a = (-R - base[c]) / lc, b = (1.0 + R - base[c]) / lc;
+        olo = fmax(olo, fmin(a, b));
+        ohi = fmin(ohi, fmax(a, b));
+      }
+    }
+    if (empty || olo > ohi) {
+      w_lo = n;
+      w_hi = -1;
+    } else {
+      const double kf = fmin(fmax((olo - L.d_min) / spacing - 0.5, -8.0 - P.write_below), n + 8.0);
+      const double kl = fmin(fmax((ohi - L.d_min) / spacing - 0.5, -8.0), n + 8.0 + P.write_above);
+      w_lo = max(0, (int)floor(kf) - 2 - P.write_below);
+      w_hi = min(n - 1, (int)ceil(kl) + 2 + P.write_above);
+    }
+  }
+  auto writes = [&](int kk) { return owner && kk >= w_lo && kk <= w_hi; };
+  const int kA = __reduce_min_sync(0xffffffffu, k_lo <= k_hi ? k_lo : n);
+  const int kB = __reduce_max_sync(0xffffffffu, k_lo <= k_hi ? k_hi : -1);
+  // before the warp's range: T = 1 on every lane (and its right neighbour)
+  const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
+  const int pre_end = kA > kB ? n : kA - 1;  // quads 0 .. kA-2 hold layers < kA only
+  if (owner)
+    for (int kk = max(0, w_lo), e = min(pre_end, w_hi + 1); kk < e; ++kk) row[(size_t)kk * ks + x] = ones;
+  if (kA > kB) return;
+  auto emit_w = [&](int kk, float a, float b) {  // all lanes shuffle; stores only where written
+    float ra = __shfl_down_sync(0xffffffffu, a, 1), rb = __shfl_down_sync(0xffffffffu, b, 1);
+    if (x == L.width - 1) {
+      ra = a;
+      rb = b;
+    }
+    if (writes(kk)) row[(size_t)kk * ks + x] = make_float4(a, b, ra, rb);
+  };
+  prev = 1.0f;
+  int k = kA;
   // SBRC_BUILD_UNROLL slices at a time: the gathers of all of them are issued
   // before any is combined (the product order of T is unchanged, so the
   // result stays bit-exact).
   constexpr int U = SBRC_BUILD_UNROLL;
-  for (; k + U <= L.n_slices; k += U) {
+  for (; k + U <= kB + 1; k += U) {
     bool cov[U];
     Cell<VT> cl[U];
 #pragma unroll
@@ -104,21 +176,33 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const float st = step_slice(cov[u], cl[u]);
-      if (k + u > 0) emit(row + (size_t)(k + u - 1) * ks, prev, st);
+      if (k + u > 0) emit_w(k + u - 1, prev, st);
       prev = st;
     }
   }
-  for (; k < L.n_slices; ++k) {
+  for (; k <= kB; ++k) {
     double ax, ay, az;
     point(k, ax, ay, az);
     const bool ca = in_cube(ax, ay, az);
     Cell<VT> la;
     if (ca) cell_fetch<VT, UNIT>(P.volume, ax, ay, az, la);
     const float sa = step_slice(ca, la);
-    if (k > 0) emit(row + (size_t)(k - 1) * ks, prev, sa);
+    if (k > 0) emit_w(k - 1, prev, sa);
     prev = sa;
   }
-  emit(row + (size_t)(L.n_slices - 1) * ks, prev, prev);
+  if (k == n) {
+    emit_w(n - 1, prev, prev);
+    return;
+  }
+  // after the warp's range: every later slice stores the final T
+  const float tc = (float)T;
+  emit_w(k - 1, prev, tc);
+  float tr = __shfl_down_sync(0xffffffffu, tc, 1);
+  if (x == L.width - 1) tr = tc;
+  const float4 tail = make_float4(tc, tc, tr, tr);
+  if (owner)
+    for (int e = min(n - 1, w_hi); k <= e; ++k)
+      if (k >= w_lo) row[(size_t)k * ks + x] = tail;
 }
 
 // Repack a plain stack into quads (one thread per texel, loop over layers).
@@ -478,6 +562,7 @@ int sbrc_build(const sbrc_build_params* p, void* stream) {
   if (p->row_begin < 0 || p->row_end > p->light.height || p->row_begin >= p->row_end) return SBRC_EINVAL;
   if (p->quad_layer_stride < 1 || p->quad_row_stride < p->light.width) return SBRC_EINVAL;
   if (p->compensation_n < 0.0) return SBRC_EINVAL;
+  if (p->write_sparse && (!(p->write_reach >= 0.0) || p->write_below < 0 || p->write_above < 0)) return SBRC_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (p->volume.voxel_type) {
     case SBRC_VOXEL_F32: launch_build<SBRC_VOXEL_F32>(*p, s); break;

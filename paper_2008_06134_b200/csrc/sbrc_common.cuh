@@ -366,6 +366,25 @@ __device__ __forceinline__ QuadTex make_quad_tex(const sbrc_render_params& P) {
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b, fmaf(-t, a, a)); }
 
+#ifndef SBRC_PREC
+#define SBRC_PREC 0  // experiment: 0 exact float64 sample path; 1 float32 colour; 2 float32 sample
+#endif
+template <int VT>
+__device__ __forceinline__ float voxel_f(typename Voxel<VT>::T x, const float* u8tab) {
+  if constexpr (VT == SBRC_VOXEL_F32) return x;
+  else return (float)Voxel<VT>::cvt(x, u8tab);
+}
+// Trilinear in float32 from the float64-placed cell (fractions rounded to float).
+template <int VT>
+__device__ __forceinline__ float cell_combine_f(const Cell<VT>& cl, const float* u8tab) {
+  const float fx = (float)cl.f[0], fy = (float)cl.f[1], fz = (float)cl.f[2];
+  const float c00 = lerpf(voxel_f<VT>(cl.r[0], u8tab), voxel_f<VT>(cl.r[1], u8tab), fx);
+  const float c10 = lerpf(voxel_f<VT>(cl.r[2], u8tab), voxel_f<VT>(cl.r[3], u8tab), fx);
+  const float c01 = lerpf(voxel_f<VT>(cl.r[4], u8tab), voxel_f<VT>(cl.r[5], u8tab), fx);
+  const float c11 = lerpf(voxel_f<VT>(cl.r[6], u8tab), voxel_f<VT>(cl.r[7], u8tab), fx);
+  return lerpf(lerpf(c00, c10, fy), lerpf(c01, c11, fy), fz);
+}
+
 // lookup_light_scalar_many at one point (lightbuffer.py:256-287): 1 outside
 // the footprint (:268-269); linear: bilinear in the two layers bracketing
 // plane-centred coordinate li, blended (:277-285); nearest: one layer
@@ -478,6 +497,12 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
   static_assert(G == 1 || SHADING == SBRC_SHADE_SHADOW || SHADING == SBRC_SHADE_SHELL || SHADING == SBRC_SHADE_CONE,
                 "ray groups carry float32 light factors (buffer modes)");
   __shared__ double2 lut[SBRC_LUT_SIZE * 2];  // 256 x rgba float64
+#if SBRC_PREC
+  __shared__ float4 lutf[SBRC_LUT_SIZE];
+  for (int i = threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x)
+    lutf[i] = make_float4((float)P.lut_rgba[4 * i], (float)P.lut_rgba[4 * i + 1], (float)P.lut_rgba[4 * i + 2],
+                          (float)P.lut_rgba[4 * i + 3]);
+#endif
   __shared__ ShellTap shell_taps[SBRC_MAX_SHELLS * 3];
   __shared__ float2 cone_cs[SBRC_MAX_ANGLES];
   __shared__ double u8tab[256];
@@ -671,6 +696,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         jf = (float)gl;
       }
       double cr = 0.0, cg = 0.0, cb = 0.0, alpha = 0.0;
+      float crf = 0.f, cgf = 0.f, cbf = 0.f, alphaf = 0.f;
+      (void)alphaf;
       // Front-to-back march (raycaster.py:428-439): the live test precedes
       // each sample, so the sample that crosses the threshold is kept.
       // the voxel cell of sample j+1 is gathered while sample j is shaded
@@ -824,6 +851,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
           fill_in = in_cube(qx, qy, qz);
           if (fill_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, fill);
         }
+#if SBRC_PREC == 0
         const double s = use_in ? cell_combine<VT>(use, reinterpret_cast<const float*>(u8tab)) : 0.0;
         const LutPos q = lut_pos(s);
         const double2 a_rg = lut[2 * q.i0], a_ba = lut[2 * q.i0 + 1];
@@ -842,6 +870,36 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         cg = dadd(cg, dmul(dmul(one_m, sg), fg));
         cb = dadd(cb, dmul(dmul(one_m, sb), fb));
         alpha = dadd(alpha, dmul(one_m, sa));
+#elif SBRC_PREC == 1
+        const double s = use_in ? cell_combine<VT>(use, reinterpret_cast<const float*>(u8tab)) : 0.0;
+        const LutPos q = lut_pos(s);
+        const double sa = dadd(dmul(lut[2 * q.i0 + 1].y, q.g), dmul(lut[2 * q.i1 + 1].y, q.f));
+        const float ff = (float)q.f;
+        const float4 c0 = lutf[q.i0], c1 = lutf[q.i1];
+        double fr = 1.0, fg = 1.0, fb = 1.0;
+        if (!SKIP || !(q.t <= clear_t)) light_factor(fr, fg, fb);
+        const double one_m = dsub(1.0, alpha);
+        const float om = (float)one_m;
+        crf = fmaf(om * lerpf(c0.x, c1.x, ff), (float)fr, crf);
+        cgf = fmaf(om * lerpf(c0.y, c1.y, ff), (float)fg, cgf);
+        cbf = fmaf(om * lerpf(c0.z, c1.z, ff), (float)fb, cbf);
+        alpha = dadd(alpha, dmul(one_m, sa));
+#else
+        const float s = use_in ? cell_combine_f<VT>(use, reinterpret_cast<const float*>(u8tab)) : 0.0f;
+        const float lt = __saturatef(s) * 255.0f;
+        const FloorF lfl = floor_f(lt);
+        const int i0 = lfl.i, i1 = min(lfl.i + 1, SBRC_LUT_SIZE - 1);
+        const float ff = lt - lfl.f;
+        const float4 c0 = lutf[i0], c1 = lutf[i1];
+        double fr = 1.0, fg = 1.0, fb = 1.0;
+        if (!SKIP || !(lt <= (float)clear_t)) light_factor(fr, fg, fb);
+        const float om = 1.0f - alphaf;
+        crf = fmaf(om * lerpf(c0.x, c1.x, ff), (float)fr, crf);
+        cgf = fmaf(om * lerpf(c0.y, c1.y, ff), (float)fg, cgf);
+        cbf = fmaf(om * lerpf(c0.z, c1.z, ff), (float)fb, cbf);
+        alphaf = fmaf(om, lerpf(c0.w, c1.w, ff), alphaf);
+        alpha = alphaf;
+#endif
         t = tn;
         jf += 1.0f;
         ++samples;
@@ -920,6 +978,13 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
           jf += (float)G;
         }
       }
+#if SBRC_PREC
+      if constexpr (G == 1) {
+        cr = crf;
+        cg = cgf;
+        cb = cbf;
+      }
+#endif
       result = make_float4((float)cr, (float)cg, (float)cb, (float)alpha);
     }
   }

@@ -32,7 +32,7 @@ import torch.distributed as dist
 
 from . import _native as N
 from .device import DeviceVolume, device_volume, f64_tensor, render_params, current_stream_handle, tile_order_for
-from .lightbuffer import build_into, check_frame
+from .lightbuffer import build_into, check_frame, lookup_reach
 
 
 def band_layout(height: int, band_rows: int, world: int):
@@ -108,7 +108,7 @@ class FrameRenderer:
 
     def __init__(self, volume, tf, light_cam, spec, settings, *, group=None, build: str = "replicated",
                  band_rows: int = 8, compensation_n: float = 0.0, device=None, assemble: str = "nccl",
-                 heavy_first: bool | None = None, feedback: bool | None = None):
+                 heavy_first: bool | None = None, feedback: bool | None = None, sparse: bool = True):
         check_frame(light_cam, spec)
         if build not in ("replicated", "sharded"):
             raise ValueError(f"build must be 'replicated' or 'sharded', got {build!r}")
@@ -131,6 +131,8 @@ class FrameRenderer:
             feedback = self.world > 1 and heavy_first is not False
         self.feedback = TileFeedback() if feedback else None
         self.band_rows, self.comp = band_rows, compensation_n
+        # sparse K1: write only the quads this march's lookups can read (lightbuffer.lookup_reach)
+        self.sparse = sparse
         # K2 params per (quads buffer, p2p raster parity); the structs own what they point to
         self._params: dict = {}
         self.lut_host = tf.resolve(settings.step)
@@ -232,6 +234,7 @@ class FrameRenderer:
             self.set_light(cam, spec)
         self.cam, self.spec, self.alpha, self.offsets = cam, spec, alpha, offsets
         self._params.clear()
+        self._complete = False
 
     def set_light(self, light_cam, spec) -> None:
         """(Re)allocate the attenuation buffer for a light frame (config 5 moves the light)."""
@@ -252,14 +255,38 @@ class FrameRenderer:
             self.shard_rows = (b, e)
             self.shard = torch.empty((hs, n, w, 4), dtype=torch.float32, device=self.dev)
             self.quads = self.storage[:h].permute(1, 0, 2, 3)  # (n, H, W, 4) view
-        self.intensity = self.quads[..., 0]
         self._params.clear()
+        self._complete = False
 
     # -------------------------------------------------------------- stages
+    @property
+    def reach(self):
+        """Lookup reach of this renderer's march (None: full K1 writes)."""
+        if not self.sparse:
+            return None
+        return lookup_reach(self.settings, self.cam, self.spec, float(self.dvol.voxel_size.max()))
+
+    @property
+    def intensity(self) -> torch.Tensor:
+        """(n, H, W) CUDA view of the current stack, complete: after a sparse
+        build the unwritten quads are filled by a full K1 into the same
+        storage first (identical values)."""
+        if not self._complete:
+            if self.shard is None:
+                build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, self.quads, self.comp)
+            else:
+                self.build()
+            self._complete = True
+        return self.quads[..., 0]
+
     def build(self) -> None:
         if self.shard is None:
-            build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, self.quads, self.comp)
+            reach = self.reach
+            build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, self.quads, self.comp,
+                       sparse=reach)
+            self._complete = reach is None
             return
+        self._complete = True
         b, e = self.shard_rows
         if e > b:
             view = self.shard[: e - b].permute(1, 0, 2, 3)  # (n, rows, W, 4), row stride n*W quads
@@ -362,7 +389,7 @@ class FramePipeline:
         fr = self.fr
         with torch.cuda.stream(self.build_stream):
             self.build_stream.wait_event(self.released[i])
-            build_into(fr.dvol, fr.alpha, fr.cam, fr.spec, fr.offsets, self.bufs[i], fr.comp)
+            build_into(fr.dvol, fr.alpha, fr.cam, fr.spec, fr.offsets, self.bufs[i], fr.comp, sparse=fr.reach)
             self.built[i].record(self.build_stream)
 
     def step(self, count_samples: bool = False) -> torch.Tensor:
@@ -374,6 +401,7 @@ class FramePipeline:
         main = torch.cuda.current_stream(fr.dev)
         main.wait_event(self.built[i])
         fr.quads = self.bufs[i]  # the renderer keeps one params struct per buffer
+        fr._complete = fr.reach is None
         fr.march(count_samples)
         self.released[i].record(main)
         img = fr.assemble()

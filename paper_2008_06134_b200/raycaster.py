@@ -26,13 +26,15 @@ import torch
 from . import _native as N
 from .device import (_require_cuda, current_stream_handle, device_volume, f64_tensor, light_frame, pack_quads,
                      quad_strides, render_params, tile_order_for, to_host)
-from .lightbuffer import AttenuationBuffer
+from .lightbuffer import AttenuationBuffer, lookup_reach
 from .scene import BUFFER_MODES, ConfigError
 
 
-def _quads_of(buffer, dev) -> torch.Tensor:
+def _quads_of(buffer, dev, need=False) -> torch.Tensor:
+    """Device quads of ``buffer``; ``need`` is the march's lookup reach
+    (a sparse buffer that covers it is used as is), False = the full stack."""
     if isinstance(buffer, AttenuationBuffer):
-        return buffer.device_quads(dev)
+        return buffer.device_quads(dev) if need is False else buffer.quads_for(need, dev)
     # a reference AttenuationBuffer (numpy intensity): upload and pack
     return pack_quads(torch.from_numpy(np.ascontiguousarray(buffer.intensity, dtype=np.float32)).to(dev))
 
@@ -50,7 +52,8 @@ def _prepare(v, tf, settings, buffer, device):
     lut = f64_tensor(lut_host, dev)
     inten, cam, spec, color = None, None, None, None
     if mode in BUFFER_MODES:
-        inten = _quads_of(buffer, dev)
+        need = lookup_reach(settings, buffer.camera, buffer.spec, float(dvol.voxel_size.max()))
+        inten = _quads_of(buffer, dev, need)
         cam, spec, color = buffer.camera, buffer.spec, buffer.camera.light_color
         n, hh, ww = inten.shape[:3]
         if (n, hh, ww) != (int(spec.n_slices), int(cam.resolution[1]), int(cam.resolution[0])):
