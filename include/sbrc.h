@@ -123,7 +123,11 @@ typedef struct sbrc_build_params {
   double write_reach;
   int32_t write_below, write_above;
   int32_t write_sparse;
-  int32_t reserved;
+  /* output_plain = 1: write the plain float32 stack I[k][y][x] instead of
+   * texel quads (strides then in float units) — the row shards a sharded
+   * multi-GPU build exchanges (4x fewer bytes than quads), packed into quads
+   * afterwards with sbrc_pack_quads. */
+  int32_t output_plain;
 } sbrc_build_params;
 
 typedef struct sbrc_render_params {

@@ -54,7 +54,7 @@ class SbrcBuildParams(C.Structure):
                 ("compensation_n", C.c_double), ("row_begin", C.c_int32), ("row_end", C.c_int32),
                 ("quads", C.c_void_p), ("quad_layer_stride", C.c_int64), ("quad_row_stride", C.c_int64),
                 ("write_reach", C.c_double), ("write_below", C.c_int32), ("write_above", C.c_int32),
-                ("write_sparse", C.c_int32), ("reserved", C.c_int32)]
+                ("write_sparse", C.c_int32), ("output_plain", C.c_int32)]
 
 
 class SbrcRenderParams(C.Structure):

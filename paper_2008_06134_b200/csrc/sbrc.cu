@@ -55,7 +55,13 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
 
   const bool comp = P.compensation_n > 0.0;
   float4* row = reinterpret_cast<float4*>(P.quads) + (size_t)(y - P.row_begin) * (size_t)P.quad_row_stride;
+  float* prow = reinterpret_cast<float*>(P.quads) + (size_t)(y - P.row_begin) * (size_t)P.quad_row_stride;
   const size_t ks = (size_t)P.quad_layer_stride;
+  const bool plain = P.output_plain != 0;
+  auto put = [&](int kk, const float4& q) {  // texel quad, or its layer-k value in the plain layout
+    if (plain) prow[(size_t)kk * ks + x] = q.x;
+    else row[(size_t)kk * ks + x] = q;
+  };
   const float* tab = reinterpret_cast<const float*>(u8tab);
   double T = 1.0;
   float prev = 0.0f;
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
   const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
   const int pre_end = kA > kB ? n : kA - 1;  // quads 0 .. kA-2 hold layers < kA only
   if (owner)
-    for (int kk = max(0, w_lo), e = min(pre_end, w_hi + 1); kk < e; ++kk) row[(size_t)kk * ks + x] = ones;
+    for (int kk = max(0, w_lo), e = min(pre_end, w_hi + 1); kk < e; ++kk) put(kk, ones);
   if (kA > kB) return;
   auto emit_w = [&](int kk, float a, float b) {  // all lanes shuffle; stores only where written
     float ra = __shfl_down_sync(0xffffffffu, a, 1), rb = __shfl_down_sync(0xffffffffu, b, 1);
@@ -155,7 +161,7 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
       ra = a;
       rb = b;
     }
-    if (writes(kk)) row[(size_t)kk * ks + x] = make_float4(a, b, ra, rb);
+    if (writes(kk)) put(kk, make_float4(a, b, ra, rb));
   };
   prev = 1.0f;
   int k = kA;
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
   const float4 tail = make_float4(tc, tc, tr, tr);
   if (owner)
     for (int e = min(n - 1, w_hi); k <= e; ++k)
-      if (k >= w_lo) row[(size_t)k * ks + x] = tail;
+      if (k >= w_lo) put(k, tail);
 }
 
 // Repack a plain stack into quads (one thread per texel, loop over layers).

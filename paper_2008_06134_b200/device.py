@@ -205,11 +205,19 @@ def quad_strides(quads: torch.Tensor) -> tuple[int, int]:
 
 
 def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, quads: torch.Tensor,
-                 compensation_n: float, row_begin: int, row_end: int, sparse=None) -> N.SbrcBuildParams:
+                 compensation_n: float, row_begin: int, row_end: int, sparse=None,
+                 plain: bool = False) -> N.SbrcBuildParams:
     """``quads`` is the (n, row_end-row_begin, W, 4) texel-quad view of the rows built;
     ``sparse`` = (reach_world, layers_below, layers_above) writes only the quads a
-    march with that lookup reach can read (lightbuffer.lookup_reach), None all."""
-    qk, qy = quad_strides(quads)
+    march with that lookup reach can read (lightbuffer.lookup_reach), None all.
+    ``plain``: ``quads`` is instead an (n, rows, W) float32 view that receives
+    the plain stack (the row shard of a sharded build)."""
+    if plain:
+        if quads.dtype != torch.float32 or quads.dim() != 3 or quads.stride(2) != 1:
+            raise ValueError("a plain stack must be an (n, rows, W) float32 view with contiguous rows")
+        qk, qy = quads.stride(0), quads.stride(1)
+    else:
+        qk, qy = quad_strides(quads)
     p = N.SbrcBuildParams()
     p.volume = dvol.struct()
     p.light = light_frame(cam, spec, offsets_dev)
@@ -217,6 +225,7 @@ def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, quad
     p.compensation_n = float(compensation_n)
     p.row_begin, p.row_end = int(row_begin), int(row_end)
     p.quads, p.quad_layer_stride, p.quad_row_stride = quads.data_ptr(), qk, qy
+    p.output_plain = int(bool(plain))
     if sparse is not None:
         p.write_sparse = 1
         p.write_reach, p.write_below, p.write_above = float(sparse[0]), int(sparse[1]), int(sparse[2])

@@ -14,11 +14,11 @@ Partitioning:
   chunk and one ``all_gather_into_tensor`` + row permutation assembles the
   raster image on every rank.
 - Build: either replicated (every rank runs the full K1; no collective) or
-  row-sharded: rank r builds light rows [r*Hs, (r+1)*Hs) into a row-major
-  [H][n][W] texel-quad buffer, whose row shards are contiguous, and one all-gather
-  replicates the full buffer. Texels are independent in the reference build
-  (lightbuffer.py:168-198), so the sharded build needs no halo; K2 reads the
-  gathered buffer through strides, so no permutation pass is needed.
+  row-sharded: rank r builds light rows [r*Hs, (r+1)*Hs) of the plain float32
+  stack into a row-major [H][n][W] buffer, whose row shards are contiguous,
+  one all-gather replicates it (A bytes, not the 4A of texel quads), and each
+  rank packs it into quads locally. Texels are independent in the reference
+  build (lightbuffer.py:168-198), so the sharded build needs no halo.
 - Volume: replicated (uploaded or broadcast once per dataset).
 """
 
@@ -31,7 +31,8 @@ import torch
 import torch.distributed as dist
 
 from . import _native as N
-from .device import DeviceVolume, device_volume, f64_tensor, render_params, current_stream_handle, tile_order_for
+from .device import (DeviceVolume, current_stream_handle, device_volume, f64_tensor, pack_quads, render_params,
+                     tile_order_for)
 from .lightbuffer import build_into, check_frame, lookup_reach
 
 
@@ -244,17 +245,17 @@ class FrameRenderer:
         self.offsets = f64_tensor(spec.plane_offsets, self.dev)
         n, h, w = int(spec.n_slices), int(light_cam.resolution[1]), int(light_cam.resolution[0])
         self._shape = (n, h, w)
+        self.storage = torch.empty((n, h, w, 4), dtype=torch.float32, device=self.dev)
+        self.quads = self.storage
         if self.build_mode == "replicated" or self.world == 1:
-            self.storage = torch.empty((n, h, w, 4), dtype=torch.float32, device=self.dev)
-            self.quads = self.storage
             self.shard = None
         else:
             b, e, hs = shard_rows(h, self.world, self.rank)
-            # row-major [H][n][W] quads: a rank's rows are one contiguous chunk
-            self.storage = torch.empty((self.world * hs, n, w, 4), dtype=torch.float32, device=self.dev)
+            # row-major [H][n][W] plain stack: a rank's rows are one contiguous chunk;
+            # the gathered stack is packed into quads locally (4x fewer bytes cross NVLink)
+            self.plain = torch.empty((self.world * hs, n, w), dtype=torch.float32, device=self.dev)
             self.shard_rows = (b, e)
-            self.shard = torch.empty((hs, n, w, 4), dtype=torch.float32, device=self.dev)
-            self.quads = self.storage[:h].permute(1, 0, 2, 3)  # (n, H, W, 4) view
+            self.shard = torch.empty((hs, n, w), dtype=torch.float32, device=self.dev)
         self._params.clear()
         self._complete = False
 
@@ -289,9 +290,11 @@ class FrameRenderer:
         self._complete = True
         b, e = self.shard_rows
         if e > b:
-            view = self.shard[: e - b].permute(1, 0, 2, 3)  # (n, rows, W, 4), row stride n*W quads
-            build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, view, self.comp, b, e)
-        all_gather_into(self.storage, self.shard, self.group)
+            view = self.shard[: e - b].permute(1, 0, 2)  # (n, rows, W), row stride n*W floats
+            build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, view, self.comp, b, e, plain=True)
+        all_gather_into(self.plain, self.shard, self.group)
+        h = int(self.cam.resolution[1])
+        pack_quads(self.plain[:h].permute(1, 0, 2), self.quads)
 
     def march(self, count_samples: bool = True) -> None:
         p2p = self.assemble_mode == "p2p"

@@ -266,6 +266,34 @@ def test_sharded_layout_build_matches(sb):
     assert np.array_equal(a, b)
 
 
+def test_sharded_plain_build_then_pack_matches(sb):
+    """The sharded build's data path on one GPU: every rank's light rows of the
+    plain float32 stack into the row-major [H][n][W] buffer (output_plain),
+    then sbrc_pack_quads into texel quads — equal to the full quad build."""
+    import torch
+    from paper_2008_06134_b200.device import device_volume, f64_tensor, pack_quads
+    from paper_2008_06134_b200.lightbuffer import build_into
+    from paper_2008_06134_b200.frame import shard_rows
+    for case, world in (("blob32", 3), ("aniso_u16", 4)):
+        g = load_golden(case)
+        v, tf, cam, spec, _ = scene_from_golden(g)
+        dev = torch.device("cuda")
+        n, h, w = spec.n_slices, cam.resolution[1], cam.resolution[0]
+        hs = shard_rows(h, world, 0)[2]
+        plain = torch.full((world * hs, n, w), float("nan"), dtype=torch.float32, device=dev)
+        alpha = f64_tensor(tf.resolve(spec.spacing)[:, 3], dev)
+        offs = f64_tensor(spec.plane_offsets, dev)
+        for r in range(world):
+            b, e, _ = shard_rows(h, world, r)
+            if e > b:
+                build_into(device_volume(v, dev), alpha, cam, spec, offs, plain[b:e].permute(1, 0, 2), 0.0, b, e,
+                           plain=True)
+        stack = plain[:h].permute(1, 0, 2)
+        assert np.array_equal(stack.cpu().numpy(), g["intensity"])
+        quads = pack_quads(stack)
+        assert torch.equal(quads, sb.build_attenuation_buffer(v, tf, cam, spec).device_quads())
+
+
 def test_pack_quads_matches_build(sb):
     """A host (reference-built) stack packed on the device equals the quads K1 writes."""
     import torch
