@@ -195,6 +195,12 @@ typedef struct sbrc_render_params {
 /* ABI version of the loaded library (== SBRC_ABI_VERSION). */
 int sbrc_abi_version(void);
 
+/* Bounds-check counters of a checked build (compiled with SBRC_CHECKED=1):
+ * out-of-extent accesses by kind (volume, quad read, quad/plain write,
+ * image, peer image, tile table, LUT index, plane offset); reset != 0 zeroes
+ * them. SBRC_EUNSUPPORTED in normal builds. Debugging aid, not on the path. */
+int sbrc_debug_violations(unsigned int counts[8], int reset);
+
 /* Human-readable text for a status code (static storage). */
 const char* sbrc_strerror(int status);
 

@@ -31,7 +31,7 @@ EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume
            "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_shadow_oracle", "sbrc_light_factor",
            "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_ipc_alloc", "sbrc_ipc_free", "sbrc_ipc_handle",
            "sbrc_ipc_open", "sbrc_ipc_close", "sbrc_march_grid", "sbrc_local_rows",
-           "sbrc_render_grid", "sbrc_host_device_pointer")
+           "sbrc_render_grid", "sbrc_host_device_pointer", "sbrc_debug_violations")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -115,6 +115,7 @@ def _load() -> C.CDLL:
     lib.sbrc_ipc_close.argtypes = [C.c_void_p]
     lib.sbrc_half_angle.argtypes = [C.POINTER(SbrcHalfAngleParams), C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(C.c_int), C.c_void_p]
+    lib.sbrc_debug_violations.argtypes = [C.POINTER(C.c_uint * 8), C.c_int]
     lib.sbrc_normalize_f32.argtypes = [C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_void_p]
     lib.sbrc_shadow_oracle.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_double, C.c_void_p, C.c_void_p]

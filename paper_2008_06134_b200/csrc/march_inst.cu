@@ -10,3 +10,5 @@
 void SBRC_MARCH_FN(SBRC_INST_SHADE, SBRC_INST_VT)(const sbrc_render_params& p, cudaStream_t s) {
   launch_march_lookup<SBRC_INST_SHADE, SBRC_INST_VT>(p, s);
 }
+
+int SBRC_MARCH_VIOL(SBRC_INST_SHADE, SBRC_INST_VT)(unsigned int* acc, int reset) { return tu_violations(acc, reset); }

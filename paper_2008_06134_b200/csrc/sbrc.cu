@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
   const size_t ks = (size_t)P.quad_layer_stride;
   const bool plain = P.output_plain != 0;
   auto put = [&](int kk, const float4& q) {  // texel quad, or its layer-k value in the plain layout
+    SBRC_CHECK(kk >= 0 && kk < L.n_slices && x < L.width && y < P.row_end, 2);
     if (plain) prow[(size_t)kk * ks + x] = q.x;
     else row[(size_t)kk * ks + x] = q;
   };
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
   };
   // pts = base + offset_k * L (:182); covered = all(0 <= pts <= 1) (:183)
   auto point = [&](int k, double& px, double& py, double& pz) {
+    SBRC_CHECK(k >= 0 && k < L.n_slices, 7);
     const double off = __ldg(L.plane_offsets + k);
     px = dadd(base[0], dmul(off, L.light_dir[0]));
     py = dadd(base[1], dmul(off, L.light_dir[1]));
@@ -470,6 +472,21 @@ void launch_build(const sbrc_build_params& p, cudaStream_t s) {
 extern "C" {
 
 int sbrc_abi_version(void) { return SBRC_ABI_VERSION; }
+
+int sbrc_debug_violations(unsigned int counts[8], int reset) {
+  if (counts == nullptr) return SBRC_EINVAL;
+  for (int i = 0; i < 8; ++i) counts[i] = 0;
+  int st = tu_violations(counts, reset);
+  if (st != SBRC_OK) return st;
+  using viol_fn = int (*)(unsigned int*, int);
+#define SBRC_VIOL_ROW(SH) SBRC_MARCH_VIOL(SH, 0), SBRC_MARCH_VIOL(SH, 1), SBRC_MARCH_VIOL(SH, 2)
+  static const viol_fn kViol[] = {SBRC_VIOL_ROW(0), SBRC_VIOL_ROW(1), SBRC_VIOL_ROW(2),
+                                  SBRC_VIOL_ROW(3), SBRC_VIOL_ROW(4), SBRC_VIOL_ROW(5)};
+#undef SBRC_VIOL_ROW
+  for (viol_fn f : kViol)
+    if ((st = f(counts, reset)) != SBRC_OK) return st;
+  return SBRC_OK;
+}
 
 const char* sbrc_strerror(int status) {
   switch (status) {

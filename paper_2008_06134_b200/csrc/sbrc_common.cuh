@@ -69,6 +69,30 @@
 #define SBRC_BUILD_UNROLL 2  // slices whose gathers are in flight together in K1
 #endif
 
+// Checked build (SBRC_CHECKED=1, scripts/checked_run.py): every global
+// read/write index of the kernels is compared with the extent of its
+// buffer and every violation counted by kind in sbrc_violations (the bad
+// access itself still happens as in the normal build, so nothing changes
+// but the count). compute-sanitizer is closed on this GPU pool; this is the
+// bounds evidence instead. Kinds: 0 volume, 1 quad read, 2 quad/plain write,
+// 3 image write, 4 peer-image write, 5 tile table, 6 LUT index, 7 plane offset.
+#ifndef SBRC_CHECKED
+#define SBRC_CHECKED 0
+#endif
+#if SBRC_CHECKED
+// one counter array per translation unit (no relocatable device code):
+// sbrc_debug_violations sums the copies of every unit
+static __device__ unsigned int sbrc_violations[8];
+#define SBRC_CHECK(cond, kind)                                                \
+  do {                                                                        \
+    if (!(cond)) atomicAdd(&sbrc_violations[kind], 1u);                       \
+  } while (0)
+#else
+#define SBRC_CHECK(cond, kind) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace {
 
 
@@ -160,6 +184,7 @@ __device__ __forceinline__ void cell_fetch(const sbrc_volume& v, double px, doub
       (unsigned)lo[2] < (unsigned)(v.nz - 1)) {
     // interior: the 2x2x2 cell without clamping
     const T* c = base + ((unsigned)lo[0] + nx * (unsigned)lo[1] + nxy * (unsigned)lo[2]);
+    SBRC_CHECK((unsigned long long)(c - base) + nxy + nx + 1 < (unsigned long long)nxy * (unsigned)v.nz, 0);
     const T* cy = c + nx;
     const T* cz = c + nxy;
     const T* cyz = cz + nx;
@@ -174,6 +199,7 @@ __device__ __forceinline__ void cell_fetch(const sbrc_volume& v, double px, doub
       b[c] = (unsigned)min(max(lo[c] + 1, 0), dims[c] - 1);
     }
     const unsigned z0 = a[2] * nxy, z1 = b[2] * nxy, y0 = a[1] * nx, y1 = b[1] * nx;
+    SBRC_CHECK((unsigned long long)z1 + y1 + b[0] < (unsigned long long)nxy * (unsigned)v.nz, 0);
     cl.r[0] = __ldg(base + (z0 + y0 + a[0])); cl.r[1] = __ldg(base + (z0 + y0 + b[0]));
     cl.r[2] = __ldg(base + (z0 + y1 + a[0])); cl.r[3] = __ldg(base + (z0 + y1 + b[0]));
     cl.r[4] = __ldg(base + (z1 + y0 + a[0])); cl.r[5] = __ldg(base + (z1 + y0 + b[0]));
@@ -226,6 +252,7 @@ __device__ __forceinline__ LutPos lut_pos(double s) {
   r.t = t;
   r.i0 = fl.i;
   r.i1 = min(r.i0 + 1, SBRC_LUT_SIZE - 1);
+  SBRC_CHECK(r.i0 >= 0 && r.i0 < SBRC_LUT_SIZE, 6);
   r.f = dsub(t, fl.f);
   r.g = dsub(1.0, r.f);
   return r;
@@ -341,6 +368,9 @@ struct QuadTex {
   float txmax, tymax;    // footprint: u in [0,1]  <=>  tx in [-0.5, W-0.5]
   float xa_max, ya_max;  // max(W-2, 0), max(H-2, 0)
   float li_max, ka_max;  // n-1, max(n-2, 0)
+#if SBRC_CHECKED
+  unsigned long long last;  // largest valid quad offset
+#endif
 };
 
 // The row steps come from the 64-bit parameter, so the compiler cannot fold
@@ -361,6 +391,9 @@ __device__ __forceinline__ QuadTex make_quad_tex(const sbrc_render_params& P) {
   t.ya_max = (float)max(LF.height - 2, 0);
   t.li_max = (float)(LF.n_slices - 1);
   t.ka_max = (float)max(LF.n_slices - 2, 0);
+#if SBRC_CHECKED
+  t.last = (unsigned long long)(LF.n_slices - 1) * t.qk + (unsigned long long)(LF.height - 1) * t.qy + LF.width - 1;
+#endif
   return t;
 }
 
@@ -409,6 +442,7 @@ __device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float 
     f = li - ka;
   }
   const float4* p = t.q + ((unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa);
+  SBRC_CHECK((unsigned long long)(p - t.q) + t.qy1_64 <= t.last && ka >= 0.f && ya >= 0.f && xa >= 0.f, 1);
   const float4 r0 = __ldg(p);
   const float4 r1 = __ldg(p + t.qy1_64);
   const float a0 = lerpf(r0.x, r0.z, fx), a1 = lerpf(r1.x, r1.z, fx);  // layer ka, rows y, y+1
@@ -427,6 +461,7 @@ __device__ __forceinline__ void interior_tap(const QuadTex& t, unsigned kbase, f
   const FloorF xl = floor_f(tx), yl = floor_f(ty);
   const float fx = tx - xl.f, fy = ty - yl.f;
   const float4* p = t.q + (kbase + (unsigned)yl.i * t.qy + (unsigned)xl.i);
+  SBRC_CHECK(p >= t.q && (unsigned long long)(p - t.q) + t.qy64 <= t.last, 1);
   const float4 r0 = __ldg(p);
   const float4 r1 = __ldg(p + t.qy64);
   v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
@@ -578,7 +613,9 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
   const int ray = lane / G, gl = lane % G;
   int bx = blockIdx.x, by = blockIdx.y;
   if (P.tile_order != nullptr) {  // heavy-first dispatch: this block renders tile tile_order[b]
+    SBRC_CHECK((int)(blockIdx.y * gridDim.x + blockIdx.x) < P.n_tiles, 5);
     const int t = __ldg(P.tile_order + blockIdx.y * gridDim.x + blockIdx.x);
+    SBRC_CHECK(t >= 0 && t < (int)(gridDim.x * gridDim.y), 5);
     bx = t % gridDim.x;
     by = t / gridDim.x;
   }
@@ -989,12 +1026,16 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
     }
   }
   if (in_image && gl == 0) {  // background (and padding rows of a partial last band) is transparent black
+    SBRC_CHECK(lr >= 0 && px >= 0 && lr < P.local_rows && px < P.width, 3);
     if (P.image != nullptr) reinterpret_cast<float4*>(P.image)[(size_t)lr * P.width + px] = result;
     // fused assembly: the pixel goes straight into every rank's raster image
     // (peer memory over NVLink); a barrier after the kernel completes the frame
     if (valid)
       for (int i = 0; i < P.n_peers; ++i)
+      {
+        SBRC_CHECK(py >= 0 && py < P.height && px < P.width, 4);
         reinterpret_cast<float4*>(P.peer_images[i])[(size_t)py * P.width + px] = result;
+      }
   }
   if (P.n_peers > 0) __threadfence_system();
   if (P.sample_count != nullptr) {
@@ -1003,6 +1044,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
   }
   if (P.tile_steps != nullptr) {  // measured cost of this tile: its longest ray's sample count
     const unsigned int mx = __reduce_max_sync(0xffffffffu, samples);
+    SBRC_CHECK(by * (int)gridDim.x + bx < P.n_tiles, 5);
     if (lane == 0 && mx) atomicMax(P.tile_steps + (by * gridDim.x + bx), mx);
   }
 }
@@ -1114,11 +1156,34 @@ void launch_march_lookup(const sbrc_render_params& p, cudaStream_t s) {
 }
 }  // namespace
 
+// Read (and optionally reset) this translation unit's checked-build counters,
+// adding them into acc[8].
+inline int tu_violations(unsigned int* acc, int reset) {
+#if SBRC_CHECKED
+  unsigned int c[8];
+  if (cudaMemcpyFromSymbol(c, sbrc_violations, sizeof(c)) != cudaSuccess) return SBRC_ECUDA;
+  for (int i = 0; i < 8; ++i) acc[i] += c[i];
+  if (reset) {
+    const unsigned int zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(sbrc_violations, zero, sizeof(zero)) != cudaSuccess) return SBRC_ECUDA;
+  }
+  return SBRC_OK;
+#else
+  (void)acc;
+  (void)reset;
+  return SBRC_EUNSUPPORTED;
+#endif
+}
+
 // K2 dispatch for one (shading mode, voxel type): march_inst.cu compiled
 // once per pair (build.py), so the instantiations compile in parallel.
 #define SBRC_MARCH_FN_(SH, VT) sbrc_march_##SH##_##VT
 #define SBRC_MARCH_FN(SH, VT) SBRC_MARCH_FN_(SH, VT)
-#define SBRC_MARCH_DECL(SH, VT) void SBRC_MARCH_FN(SH, VT)(const sbrc_render_params& p, cudaStream_t s);
+#define SBRC_MARCH_VIOL_(SH, VT) sbrc_march_violations_##SH##_##VT
+#define SBRC_MARCH_VIOL(SH, VT) SBRC_MARCH_VIOL_(SH, VT)
+#define SBRC_MARCH_DECL(SH, VT)                                                   \
+  void SBRC_MARCH_FN(SH, VT)(const sbrc_render_params& p, cudaStream_t s);      \
+  int SBRC_MARCH_VIOL(SH, VT)(unsigned int* acc, int reset);
 #define SBRC_MARCH_DECL_VT(SH) SBRC_MARCH_DECL(SH, 0) SBRC_MARCH_DECL(SH, 1) SBRC_MARCH_DECL(SH, 2)
 SBRC_MARCH_DECL_VT(0)
 SBRC_MARCH_DECL_VT(1)
