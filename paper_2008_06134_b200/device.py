@@ -13,7 +13,9 @@ same array only re-use it.
 from __future__ import annotations
 
 import math
+import threading
 import weakref
+from collections import OrderedDict
 
 import numpy as np
 import torch
@@ -170,6 +172,54 @@ def f64_tensor(arr, device) -> torch.Tensor:
     torch's caching host allocator once the copy has completed)."""
     host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))
     return host.pin_memory().to(device, non_blocking=True)
+
+
+_CONST_CACHE: "OrderedDict" = None
+_CONST_LOCK = threading.Lock()
+
+
+def device_const(arr, device) -> torch.Tensor:
+    """Device copy of a small float64 host array (LUTs, plane offsets), cached
+    by value: a frame whose inputs did not change uploads nothing. The
+    tensors are read-only inputs of the kernels; a caller keeps the one it
+    got alive for as long as its launches need it."""
+    global _CONST_CACHE
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    key = (str(device), a.shape, a.tobytes())
+    with _CONST_LOCK:
+        if _CONST_CACHE is None:
+            _CONST_CACHE = OrderedDict()
+        t = _CONST_CACHE.get(key)
+        if t is not None:
+            _CONST_CACHE.move_to_end(key)
+            return t
+    t = f64_tensor(a, device)
+    with _CONST_LOCK:
+        _CONST_CACHE[key] = t
+        while len(_CONST_CACHE) > 256:
+            _CONST_CACHE.popitem(last=False)
+    return t
+
+
+_RESOLVED: dict = {}
+
+
+def resolved_lut(tf, step: float) -> np.ndarray:
+    """tf.resolve(step) (transfer.py:76-84), memoised by the LUT's bytes and the
+    step: the float64 power of 256 entries is recomputed only when they change.
+    The result is read-only."""
+    lut = getattr(tf, "lut", None)
+    if lut is None:
+        return tf.resolve(step)
+    key = (np.ascontiguousarray(lut).tobytes(), float(step), type(tf).resolve)
+    out = _RESOLVED.get(key)
+    if out is None:
+        out = np.asarray(tf.resolve(step))
+        out.setflags(write=False)
+        if len(_RESOLVED) > 256:
+            _RESOLVED.clear()
+        _RESOLVED[key] = out
+    return out
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:

@@ -16,7 +16,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import _require_cuda, build_params, current_stream_handle, device_volume, f64_tensor, pack_quads, to_host
+from .device import (_require_cuda, build_params, current_stream_handle, device_const, device_volume, f64_tensor,
+                     pack_quads, resolved_lut, to_host)
 
 
 class AttenuationBuffer:
@@ -183,8 +184,8 @@ def build_attenuation_buffer(v, tf, cam, spec, compensation_n: float = 0.0, devi
     w, h = int(cam.resolution[0]), int(cam.resolution[1])
     n = int(spec.n_slices)
     dvol = device_volume(v, dev)
-    alpha = f64_tensor(tf.resolve(spec.spacing)[:, 3], dev)   # :159-160
-    offsets = f64_tensor(spec.plane_offsets, dev)
+    alpha = device_const(resolved_lut(tf, spec.spacing)[:, 3], dev)   # :159-160
+    offsets = device_const(spec.plane_offsets, dev)
     quads = torch.empty((n, h, w, 4), dtype=torch.float32, device=dev)
     reach = default_reach(cam, spec, float(dvol.voxel_size.max()))
     build_into(dvol, alpha, cam, spec, offsets, quads, compensation_n, sparse=reach)

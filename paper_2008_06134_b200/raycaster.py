@@ -24,7 +24,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import (_require_cuda, current_stream_handle, device_volume, f64_tensor, light_frame, pack_quads,
+from .device import (_require_cuda, current_stream_handle, device_const, device_volume, f64_tensor, light_frame,
+                     pack_quads, resolved_lut,
                      quad_strides, render_params, tile_order_for, to_host)
 from .lightbuffer import AttenuationBuffer, lookup_reach
 from .scene import BUFFER_MODES, ConfigError
@@ -48,8 +49,8 @@ def _prepare(v, tf, settings, buffer, device):
         raise ValueError(f"unknown lookup mode {settings.lookup_mode!r}")
     dev = _require_cuda(device)
     dvol = device_volume(v, dev)
-    lut_host = tf.resolve(settings.step)   # raycaster.py:453
-    lut = f64_tensor(lut_host, dev)
+    lut_host = resolved_lut(tf, settings.step)   # raycaster.py:453
+    lut = device_const(lut_host, dev)
     inten, cam, spec, color = None, None, None, None
     if mode in BUFFER_MODES:
         need = lookup_reach(settings, buffer.camera, buffer.spec, float(dvol.voxel_size.max()))
