@@ -23,10 +23,33 @@ namespace {
 #ifndef SBRC_BUILD_MINB
 #define SBRC_BUILD_MINB 6
 #endif
-template <int VT, bool UNIT>
-__global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_kernel(const sbrc_build_params P) {
+// Async gather pipeline (float32 volumes): the 8 corner voxels of slice
+// k + D - 1 are copied global -> shared with cp.async (LDGSTS, no register
+// staging) while slice k is combined, so D - 1 slices of gathers are in
+// flight per texel instead of SBRC_BUILD_UNROLL held in registers.
+#ifndef SBRC_BUILD_ASYNC
+#define SBRC_BUILD_ASYNC 0  // A/B option: slower on config 3 (0.309 -> 0.355 ms at D = 4; profiles/r2_notes.md)
+#endif
+#ifndef SBRC_BUILD_ASYNC_MINB
+#define SBRC_BUILD_ASYNC_MINB 6
+#endif
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int VT, bool UNIT, int D>
+__global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, D > 0 ? SBRC_BUILD_ASYNC_MINB : SBRC_BUILD_MINB)
+    build_kernel(const sbrc_build_params P) {
+  static_assert(D == 0 || VT == SBRC_VOXEL_F32, "the async gather pipeline copies 4-byte voxels");
   __shared__ double lut[SBRC_LUT_SIZE];
-  __shared__ double u8tab[256];
+  __shared__ double u8tab[VT == SBRC_VOXEL_U8 ? 256 : 1];
   for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x * blockDim.y)
     lut[i] = P.alpha_lut[i];
   if (std::is_same<typename Voxel<VT>::T, unsigned char>::value) fill_u8_table(u8tab);
@@ -167,6 +190,86 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
   };
   prev = 1.0f;
   int k = kA;
+  if constexpr (D > 0) {
+    // Stage st of this thread: corner voxels svox[st][c][tid] (landed by
+    // cp.async) and the cell fractions sfr[st][a][tid] (float64, stored at
+    // issue; sfr[st][0] = -1 marks an uncovered texel-slice point). Each
+    // thread reads only its own slots, so no barrier is needed; a slot is
+    // refilled only after the thread consumed it (program order).
+    constexpr int NT = 32 * SBRC_BUILD_ROWS;
+    __shared__ float svox[D > 0 ? D : 1][8][NT];
+    __shared__ double sfr[D > 0 ? D : 1][3][NT];
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const float* vb = reinterpret_cast<const float*>(P.volume.data);
+    const int dims[3] = {P.volume.nx, P.volume.ny, P.volume.nz};
+    const unsigned nx = (unsigned)P.volume.nx, nxy = (unsigned)P.volume.nx * (unsigned)P.volume.ny;
+    auto issue = [&](int kk, int st) {
+      double p[3];
+      point(kk, p[0], p[1], p[2]);
+      if (!in_cube(p[0], p[1], p[2])) {
+        sfr[st][0][tid] = -1.0;
+        return;
+      }
+      int lo[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {  // cell_fetch's arithmetic (volume.py:175-182)
+        double local = p[c];
+        if (!UNIT) local = dclip01(ddiv(dsub(p[c], P.volume.box_lo[c]), P.volume.box_ext[c]));
+        const double g = dsub(dmul(local, (double)dims[c]), 0.5);
+        const FloorD fl = floor_d(g);
+        sfr[st][c][tid] = dsub(g, fl.f);
+        lo[c] = fl.i;
+      }
+      unsigned o[8];
+      if ((unsigned)lo[0] < nx - 1 && (unsigned)lo[1] < (unsigned)(dims[1] - 1) &&
+          (unsigned)lo[2] < (unsigned)(dims[2] - 1)) {
+        const unsigned c0 = (unsigned)lo[0] + nx * (unsigned)lo[1] + nxy * (unsigned)lo[2];
+        o[0] = c0; o[1] = c0 + 1; o[2] = c0 + nx; o[3] = c0 + nx + 1;
+        o[4] = c0 + nxy; o[5] = c0 + nxy + 1; o[6] = c0 + nxy + nx; o[7] = c0 + nxy + nx + 1;
+      } else {
+        unsigned a[3], b[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          a[c] = (unsigned)min(max(lo[c], 0), dims[c] - 1);
+          b[c] = (unsigned)min(max(lo[c] + 1, 0), dims[c] - 1);
+        }
+        const unsigned z0 = a[2] * nxy, z1 = b[2] * nxy, y0 = a[1] * nx, y1 = b[1] * nx;
+        o[0] = z0 + y0 + a[0]; o[1] = z0 + y0 + b[0]; o[2] = z0 + y1 + a[0]; o[3] = z0 + y1 + b[0];
+        o[4] = z1 + y0 + a[0]; o[5] = z1 + y0 + b[0]; o[6] = z1 + y1 + a[0]; o[7] = z1 + y1 + b[0];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        SBRC_CHECK((unsigned long long)o[c] < (unsigned long long)nxy * (unsigned)dims[2], 0);
+        cp_async4(&svox[st][c][tid], vb + o[c]);
+      }
+    };
+    int si = 0;
+    for (int j = 0; j < D - 1; ++j) {  // prologue: slices kA .. kA+D-2 in flight
+      if (kA + j <= kB) issue(kA + j, si);
+      cp_async_commit();
+      si = si == D - 1 ? 0 : si + 1;
+    }
+    int sc = 0;
+    for (; k <= kB; ++k) {
+      if (k + D - 1 <= kB) issue(k + D - 1, si);
+      cp_async_commit();
+      si = si == D - 1 ? 0 : si + 1;
+      cp_async_wait<D - 1>();  // this thread's copies of slice k have landed
+      Cell<VT> cl;
+      cl.f[0] = sfr[sc][0][tid];
+      const bool cov = cl.f[0] >= 0.0;
+      if (cov) {
+        cl.f[1] = sfr[sc][1][tid];
+        cl.f[2] = sfr[sc][2][tid];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) cl.r[c] = svox[sc][c][tid];
+      }
+      sc = sc == D - 1 ? 0 : sc + 1;
+      const float st = step_slice(cov, cl);
+      if (k > 0) emit_w(k - 1, prev, st);
+      prev = st;
+    }
+  } else {
   // SBRC_BUILD_UNROLL slices at a time: the gathers of all of them are issued
   // before any is combined (the product order of T is unchanged, so the
   // result stays bit-exact).
@@ -197,6 +300,7 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, SBRC_BUILD_MINB) build_k
     const float sa = step_slice(ca, la);
     if (k > 0) emit_w(k - 1, prev, sa);
     prev = sa;
+  }
   }
   if (k == n) {
     emit_w(n - 1, prev, prev);
@@ -463,8 +567,9 @@ template <int VT>
 void launch_build(const sbrc_build_params& p, cudaStream_t s) {
   dim3 block(32, SBRC_BUILD_ROWS);  // warps are rows of 31 owned texels (build_kernel)
   dim3 grid((p.light.width + 30) / 31, (p.row_end - p.row_begin + SBRC_BUILD_ROWS - 1) / SBRC_BUILD_ROWS);
-  if (unit_box(p.volume)) build_kernel<VT, true><<<grid, block, 0, s>>>(p);
-  else build_kernel<VT, false><<<grid, block, 0, s>>>(p);
+  constexpr int D = VT == SBRC_VOXEL_F32 ? SBRC_BUILD_ASYNC : 0;
+  if (unit_box(p.volume)) build_kernel<VT, true, D><<<grid, block, 0, s>>>(p);
+  else build_kernel<VT, false, D><<<grid, block, 0, s>>>(p);
 }
 
 }  // namespace

@@ -37,8 +37,13 @@ def main():
 
     sparse = timed(fr.build)
     full = timed(lambda: build_into(fr.dvol, fr.alpha, fr.cam, fr.spec, fr.offsets, fr.quads, fr.comp))
+    import hashlib
+    fr.quads.zero_()
+    build_into(fr.dvol, fr.alpha, fr.cam, fr.spec, fr.offsets, fr.quads, fr.comp)
+    torch.cuda.synchronize()
+    digest = hashlib.sha256(fr.quads.cpu().numpy().tobytes()).hexdigest()[:16]
     print(json.dumps({"lib": os.path.basename(N.LIB_PATH), "config": cfg_id, "k1_sparse_ms": sparse,
-                      "k1_full_ms": full}))
+                      "k1_full_ms": full, "quads_sha": digest}))
 
 
 if __name__ == "__main__":
