@@ -468,6 +468,9 @@ __device__ __forceinline__ void interior_tap(const QuadTex& t, unsigned kbase, f
   v1 += lerpf(lerpf(r0.y, r0.w, fx), lerpf(r1.y, r1.w, fx), fy);
 }
 
+#ifndef SBRC_WARP_VOTE
+#define SBRC_WARP_VOTE 0  // 1: the march loop runs while __any_sync(live) (A/B)
+#endif
 #ifndef SBRC_PACKED
 #define SBRC_PACKED 3  // shell interior taps in packed float32x2 arithmetic (FFMA2 / FADD2, sm_100)
 #endif
@@ -1002,6 +1005,24 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         jf += 1.0f;
         ++samples;
       };
+#if SBRC_WARP_VOTE
+      // Early ray termination as a warp vote: the warp steps while any lane's
+      // ray is live (raycaster.py:429 live test per lane, before each sample).
+      // The lanes that reach this loop (valid pixels whose ray hits the cube)
+      // vote among themselves.
+      const unsigned vmask = __activemask();
+      bool live = t < t_far && alpha < thresh;
+      while (__any_sync(vmask, live)) {
+        if (live) {
+          Cell<VT> nxt;
+          bool nxt_in;
+          sample(cur, cur_in, nxt, nxt_in);
+          cur = nxt;
+          cur_in = nxt_in;
+          live = t < t_far && alpha < thresh;
+        }
+      }
+#else
       while (t < t_far && alpha < thresh) {
         Cell<VT> nxt;
         bool nxt_in;
@@ -1009,6 +1030,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
         cur = nxt;
         cur_in = nxt_in;
       }
+#endif
       } else {
         // Ray group: each lane shades its own samples; the G samples of a
         // step are then composited in order by every lane of the group with
