@@ -66,7 +66,9 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--mode", default=None, help="override shading mode")
-    ap.add_argument("--build", choices=("replicated", "sharded"), default="replicated")
+    ap.add_argument("--build", choices=("replicated", "sharded", "frustum"), default="frustum",
+                    help="N > 1: full K1 per rank, row-sharded K1 + all-gather, or frustum-culled K1 per "
+                         "contiguous rank band (partition.py)")
     ap.add_argument("--assemble", choices=("p2p", "nccl"), default="p2p",
                     help="N>1 image assembly: fused peer-memory stores from the march kernel (self-checked, "
                          "falls back to NCCL) or NCCL all-gather")
@@ -508,7 +510,26 @@ def run_ours(a, cfg, mode):
         dist.all_reduce(t)
         samples = int(t.item())
 
-    pipelined = (world == 1 or a.build == "replicated") and not a.no_pipeline
+    if world > 1 and a.build == "frustum":
+        # contiguous bands re-cut from measured per-rank frame times (FrameRenderer.rebalance)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        best = None
+        for _ in range(6):
+            ev[0].record(stream)
+            for _ in range(3):
+                fr.build()
+                fr.march(count_samples=False)
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([ev[0].elapsed_time(ev[1]) / 3], dtype=torch.float64, device=dev)
+            worst = t.clone()
+            dist.all_reduce(worst, op=dist.ReduceOp.MAX)
+            if best is None or worst.item() < best[0]:
+                best = (worst.item(), list(fr.ranges))
+            fr.rebalance(t.item())
+        fr.set_ranges(best[1])
+        fr.frame()
+    pipelined = (world == 1 or a.build in ("replicated", "frustum")) and not a.no_pipeline
     pipe = FramePipeline(fr) if pipelined else None
 
     def one_step(ev=None):
@@ -582,7 +603,7 @@ def run_ours(a, cfg, mode):
     # ---- roofline of the dominant kernel
     vbytes = {0: 4, 1: 1, 2: 2}[dvol.source_type]  # algorithmic V counts the source bytes per voxel
     V, A, I = algorithmic_bytes(cfg, vbytes, world)
-    k1_bytes = V + (A if (world == 1 or a.build == "replicated") else A // world)
+    k1_bytes = V + (A if (world == 1 or a.build != "sharded") else A // world)
     k2_bytes = (V + A + I // world) if mode != "none" else (V + I // world)
     peaks = load_peaks()
     dominant = "march" if k2_ms >= k1_ms else "build"
@@ -623,6 +644,7 @@ def run_ours(a, cfg, mode):
             "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
             "config": workload_config(a, cfg, mode, world),
             "setup": {"build": a.build if world > 1 else "single",
+                      "row_ranges": fr.ranges if fr.partition == "contiguous" else None,
                       "assemble": fr.assemble_mode if world > 1 else "none",
                       "frame_pipelining": "build(f+1) overlaps march(f)" if pipelined else "off",
                       "tile_order": "measured (previous frame)" if fr.feedback is not None else

@@ -37,11 +37,12 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 9
+#define SBRC_ABI_VERSION 10
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
 #define SBRC_MAX_PEERS 8    /* GPUs of one node (image assembly over peer memory) */
+#define SBRC_MAX_CLIP 4     /* consumer clip half-spaces of a frustum-culled build */
 
 typedef enum sbrc_status {
   SBRC_OK = 0,
@@ -128,6 +129,17 @@ typedef struct sbrc_build_params {
    * multi-GPU build exchanges (4x fewer bytes than quads), packed into quads
    * afterwards with sbrc_pack_quads. */
   int32_t output_plain;
+  /* Consumer clip (frustum-culled build, write_sparse = 1 only): the march
+   * that reads this stack samples only points p with
+   * clip[i][0]*p.x + clip[i][1]*p.y + clip[i][2]*p.z + clip[i][3] >= 0 for
+   * every i < n_clip (half-spaces already widened by the lookups' lateral
+   * reach) — e.g. the two planes through the eye that bound one rank's
+   * contiguous image rows. Layers outside the clipped texel line (widened
+   * by write_below / write_above) are not written, and the slice recurrence
+   * of a warp stops after the last layer any of its texels writes: values
+   * written are identical to a full build. */
+  int32_t n_clip;
+  double clip[SBRC_MAX_CLIP][4];
 } sbrc_build_params;
 
 typedef struct sbrc_render_params {
@@ -190,6 +202,11 @@ typedef struct sbrc_render_params {
    * sample count of its longest ray into tile_steps[tile]. Sorted in
    * decreasing order it is the next frame's heavy-first tile_order. */
   unsigned int* tile_steps;
+  /* Contiguous partition (row_count > 0): this rank renders raster rows
+   * [row_begin, row_begin + row_count) into rank-local rows 0..row_count-1
+   * (band_rows / rank / world are then ignored). Used with a frustum-culled
+   * build, whose texels only cover one contiguous screen band. */
+  int32_t row_begin, row_count;
 } sbrc_render_params;
 
 /* ABI version of the loaded library (== SBRC_ABI_VERSION). */

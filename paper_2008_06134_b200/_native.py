@@ -16,10 +16,11 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
-ABI_VERSION = 9
+ABI_VERSION = 10
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 MAX_PEERS = 8
+MAX_CLIP = 4
 
 OK, EINVAL, ECONFIG, ECUDA, EUNSUPPORTED = 0, -1, -2, -3, -4
 VOXEL_F32, VOXEL_U8, VOXEL_U16 = 0, 1, 2
@@ -54,7 +55,8 @@ class SbrcBuildParams(C.Structure):
                 ("compensation_n", C.c_double), ("row_begin", C.c_int32), ("row_end", C.c_int32),
                 ("quads", C.c_void_p), ("quad_layer_stride", C.c_int64), ("quad_row_stride", C.c_int64),
                 ("write_reach", C.c_double), ("write_below", C.c_int32), ("write_above", C.c_int32),
-                ("write_sparse", C.c_int32), ("output_plain", C.c_int32)]
+                ("write_sparse", C.c_int32), ("output_plain", C.c_int32),
+                ("n_clip", C.c_int32), ("clip", (C.c_double * 4) * MAX_CLIP)]
 
 
 class SbrcRenderParams(C.Structure):
@@ -74,7 +76,7 @@ class SbrcRenderParams(C.Structure):
                 ("scene_light_dir", D3), ("phong", C.c_double * 4), ("voxel_size", D3),
                 ("image", C.c_void_p), ("peer_images", C.c_void_p * MAX_PEERS), ("n_peers", C.c_int32),
                 ("n_tiles", C.c_int32), ("tile_order", C.c_void_p), ("sample_count", C.c_void_p),
-                ("tile_steps", C.c_void_p)]
+                ("tile_steps", C.c_void_p), ("row_begin", C.c_int32), ("row_count", C.c_int32)]
 
 
 class SbrcHalfAngleParams(C.Structure):

@@ -161,6 +161,20 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, D > 0 ? SBRC_BUILD_ASYNC
         ohi = fmin(ohi, fmax(a, b));
       }
     }
+    // consumer clip half-spaces n.p + c >= 0 along the line: (n.base + c) + o (n.L) >= 0
+    for (int i = 0; i < P.n_clip; ++i) {
+      const double* h = P.clip[i];
+      const double s0 = h[0] * base[0] + h[1] * base[1] + h[2] * base[2] + h[3];
+      const double sl = h[0] * L.light_dir[0] + h[1] * L.light_dir[1] + h[2] * L.light_dir[2];
+      const double nn = fabs(h[0]) + fabs(h[1]) + fabs(h[2]);
+      if (fabs(sl) <= 1e-9 * nn) {  // plane (nearly) parallel to the light: the whole line or nothing
+        if (s0 < -1e-9 * nn) empty = true;
+      } else if (sl > 0.0) {
+        olo = fmax(olo, -s0 / sl);
+      } else {
+        ohi = fmin(ohi, -s0 / sl);
+      }
+    }
     if (empty || olo > ohi) {
       w_lo = n;
       w_hi = -1;
@@ -173,7 +187,13 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, D > 0 ? SBRC_BUILD_ASYNC
   }
   auto writes = [&](int kk) { return owner && kk >= w_lo && kk <= w_hi; };
   const int kA = __reduce_min_sync(0xffffffffu, k_lo <= k_hi ? k_lo : n);
-  const int kB = __reduce_max_sync(0xffffffffu, k_lo <= k_hi ? k_hi : -1);
+  int kB = __reduce_max_sync(0xffffffffu, k_lo <= k_hi ? k_hi : -1);
+  if (P.write_sparse && P.n_clip > 0) {
+    // the last quad any texel of the warp writes is w_hi: it needs I[w_hi + 1],
+    // the value stored at slice w_hi + 1 (T after slice w_hi) — later slices are not needed
+    const int wmax = __reduce_max_sync(0xffffffffu, owner && w_lo <= w_hi ? w_hi : -1);
+    kB = min(kB, wmax + 1);
+  }
   // before the warp's range: T = 1 on every lane (and its right neighbour)
   const float4 ones = make_float4(1.f, 1.f, 1.f, 1.f);
   const int pre_end = kA > kB ? n : kA - 1;  // quads 0 .. kA-2 hold layers < kA only
@@ -665,11 +685,17 @@ int sbrc_march_grid(int width, int height, int band_rows, int rank, int world, i
   return SBRC_OK;
 }
 
+// Row partition of a render call: a contiguous range inside the image, or
+// bands of a multiple of 8 rows dealt to rank < world.
+static bool rows_ok(const sbrc_render_params* p) {
+  if (p->row_count > 0) return p->row_begin >= 0 && p->row_begin + p->row_count <= p->height;
+  return p->row_count == 0 && p->band_rows >= 1 && p->band_rows % 8 == 0 && p->world >= 1 && p->rank >= 0 &&
+         p->rank < p->world;
+}
+
 int sbrc_render_grid(const sbrc_render_params* p, int* grid) {
-  if (p == nullptr || grid == nullptr || p->width < 1 || p->height < 1 || p->band_rows < 1 || p->world < 1 ||
-      p->rank < 0 || p->rank >= p->world)
-    return SBRC_EINVAL;
-  const MarchShape m = march_shape(*p, sbrc_local_rows(p->height, p->band_rows, p->rank, p->world));
+  if (p == nullptr || grid == nullptr || p->width < 1 || p->height < 1 || !rows_ok(p)) return SBRC_EINVAL;
+  const MarchShape m = march_shape(*p, rank_rows(*p));
   grid[0] = m.tiles_x;
   grid[1] = m.tiles_y;
   grid[2] = m.bw;
@@ -688,6 +714,7 @@ int sbrc_build(const sbrc_build_params* p, void* stream) {
   if (p == nullptr || !volume_ok(p->volume) || !light_ok(p->light)) return SBRC_EINVAL;
   if (p->light.plane_offsets == nullptr || p->alpha_lut == nullptr || p->quads == nullptr) return SBRC_EINVAL;
   if (p->row_begin < 0 || p->row_end > p->light.height || p->row_begin >= p->row_end) return SBRC_EINVAL;
+  if (p->n_clip < 0 || p->n_clip > SBRC_MAX_CLIP || (p->n_clip > 0 && !p->write_sparse)) return SBRC_EINVAL;
   if (p->quad_layer_stride < 1 || p->quad_row_stride < p->light.width) return SBRC_EINVAL;
   if (p->compensation_n < 0.0) return SBRC_EINVAL;
   if (p->write_sparse && (!(p->write_reach >= 0.0) || p->write_below < 0 || p->write_above < 0)) return SBRC_EINVAL;
@@ -801,8 +828,7 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
     if (p->peer_images[i] == nullptr) return SBRC_EINVAL;
   if (p->shading < SBRC_SHADE_NONE || p->shading > SBRC_SHADE_EXTINCTION) return SBRC_EUNSUPPORTED;
   if (p->lookup != SBRC_LOOKUP_LINEAR && p->lookup != SBRC_LOOKUP_NEAREST) return SBRC_EINVAL;
-  if (p->band_rows < 1 || p->band_rows % 8 != 0 || p->world < 1 || p->rank < 0 || p->rank >= p->world)
-    return SBRC_EINVAL;
+  if (!rows_ok(p)) return SBRC_EINVAL;
   if (p->shading >= SBRC_SHADE_SHADOW && p->shading <= SBRC_SHADE_CONE) {
     if (p->quads == nullptr) return SBRC_ECONFIG;
     if (!light_ok(p->light)) return SBRC_EINVAL;
@@ -814,7 +840,7 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
       (p->cone_axis_samples < 1 || p->cone_angle_count < 1 || p->cone_angle_count > SBRC_MAX_ANGLES ||
        p->cone_ring < 0.0))
     return SBRC_EINVAL;
-  if (sbrc_local_rows(p->height, p->band_rows, p->rank, p->world) == 0) return SBRC_OK;
+  if (rank_rows(*p) == 0) return SBRC_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   using march_fn = void (*)(const sbrc_render_params&, cudaStream_t);
 #define SBRC_MARCH_ROW(SH) {SBRC_MARCH_FN(SH, 0), SBRC_MARCH_FN(SH, 1), SBRC_MARCH_FN(SH, 2)}

@@ -669,8 +669,13 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
   }
   const int px = bx * (WX * TW) + (warp % WX) * TW + (ray % TW);
   const int lr = by * (WY * TH) + (warp / WX) * TH + (ray / TW);  // rank-local row
-  const int band = lr / P.band_rows;
-  const int py = (P.rank + band * P.world) * P.band_rows + (lr - band * P.band_rows);
+  int py;
+  if (P.row_count > 0) {  // contiguous partition
+    py = P.row_begin + lr;
+  } else {
+    const int band = lr / P.band_rows;
+    py = (P.rank + band * P.world) * P.band_rows + (lr - band * P.band_rows);
+  }
   const bool in_image = px < P.width && lr < P.local_rows;
   const bool valid = in_image && py < P.height;
 
@@ -1155,6 +1160,11 @@ inline bool quads_ok(const sbrc_light_frame& L, int64_t qk, int64_t qy) {
   return last < (1ll << 32);
 }
 
+// Rank-local image rows of a launch: the contiguous range, or the rank's bands.
+inline int rank_rows(const sbrc_render_params& p) {
+  return p.row_count > 0 ? p.row_count : sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
+}
+
 inline bool unit_box(const sbrc_volume& v) {
   for (int c = 0; c < 3; ++c)
     if (v.box_lo[c] != 0.0 || v.box_ext[c] != 1.0) return false;
@@ -1164,7 +1174,7 @@ inline bool unit_box(const sbrc_volume& v) {
 template <int SH, int LK, int VT, bool UNIT, int NS, int CA, int CN, bool SKIP>
 void launch_march_skip(const sbrc_render_params& p, cudaStream_t s) {
   sbrc_render_params q = p;
-  q.local_rows = sbrc_local_rows(p.height, p.band_rows, p.rank, p.world);
+  q.local_rows = rank_rows(p);
   // latency mode for the default kernels when the rank-local image is small
   // (A/B in profiles/r01_notes.md: 131K px/rank 1.05 -> 0.75 ms; 262K px: 1.16 vs 1.28)
   constexpr bool LAT = LK == SBRC_LOOKUP_LINEAR &&

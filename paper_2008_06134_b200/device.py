@@ -256,12 +256,14 @@ def quad_strides(quads: torch.Tensor) -> tuple[int, int]:
 
 def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, quads: torch.Tensor,
                  compensation_n: float, row_begin: int, row_end: int, sparse=None,
-                 plain: bool = False) -> N.SbrcBuildParams:
+                 plain: bool = False, clip=()) -> N.SbrcBuildParams:
     """``quads`` is the (n, row_end-row_begin, W, 4) texel-quad view of the rows built;
     ``sparse`` = (reach_world, layers_below, layers_above) writes only the quads a
     march with that lookup reach can read (lightbuffer.lookup_reach), None all.
     ``plain``: ``quads`` is instead an (n, rows, W) float32 view that receives
-    the plain stack (the row shard of a sharded build)."""
+    the plain stack (the row shard of a sharded build). ``clip``: the
+    consumer's half-spaces (a, b, c, d), a.x + b.y + c.z + d >= 0, already
+    widened by its lookup reach (partition.frustum_clip; needs ``sparse``)."""
     if plain:
         if quads.dtype != torch.float32 or quads.dim() != 3 or quads.stride(2) != 1:
             raise ValueError("a plain stack must be an (n, rows, W) float32 view with contiguous rows")
@@ -279,6 +281,14 @@ def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, quad
     if sparse is not None:
         p.write_sparse = 1
         p.write_reach, p.write_below, p.write_above = float(sparse[0]), int(sparse[1]), int(sparse[2])
+    if clip:
+        if sparse is None:
+            raise ValueError("a clipped (frustum-culled) build is a sparse build: pass the lookup reach")
+        if len(clip) > N.MAX_CLIP:
+            raise ValueError(f"at most {N.MAX_CLIP} clip half-spaces")
+        p.n_clip = len(clip)
+        for i, h in enumerate(clip):
+            p.clip[i][:] = [float(x) for x in h]
     return p
 
 
@@ -315,9 +325,11 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
                   peer_images=(), heavy_first: bool = False,
-                  lut_host: np.ndarray | None = None, feedback=None) -> N.SbrcRenderParams:
+                  lut_host: np.ndarray | None = None, feedback=None, row_range=None) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469).
-    ``lut_host`` (the resolved LUT on the host) enables the skip_clear hint."""
+    ``lut_host`` (the resolved LUT on the host) enables the skip_clear hint.
+    ``row_range`` = (row_begin, row_count): a contiguous share of the image
+    rows instead of the (band_rows, rank, world) bands."""
     mode = settings.shading_mode
     if mode not in N.SHADE:
         raise ValueError(f"unknown shading mode {mode!r}")
@@ -371,6 +383,8 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     if lut_host is not None and mode != "none":
         p.skip_clear = int(skip_clear_hint(dvol, lut_host))
     p.band_rows, p.rank, p.world = int(band_rows), int(rank), int(world)
+    if row_range is not None:
+        p.row_begin, p.row_count = int(row_range[0]), int(row_range[1])
     p.image = image.data_ptr() if image is not None else None
     if len(peer_images) > N.MAX_PEERS:
         raise ValueError(f"at most {N.MAX_PEERS} peer images")
@@ -383,7 +397,7 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     keep = [dvol.data, lut_dev, quads_dev, image, counter]
     if heavy_first:  # dispatch table over the exact grid sbrc_render will launch
         grid = N.render_grid(p)
-        order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, grid)
+        order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, grid, row_range)
         if feedback is not None:  # measured order of the previous frame (schedule.TileFeedback)
             order, steps = feedback.prepare(grid, order)
             p.tile_steps = steps.data_ptr()
@@ -397,19 +411,20 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
 _ORDER_CACHE: dict = {}
 
 
-def tile_order_for(settings, band_rows: int, rank: int, world: int, device, grid=None) -> torch.Tensor:
+def tile_order_for(settings, band_rows: int, rank: int, world: int, device, grid=None,
+                   row_range=None) -> torch.Tensor:
     """Device copy of the heavy-first dispatch table (schedule.heavy_first) over
     ``grid`` (tiles_x, tiles_y, tile_w, tile_h; default the block grid), cached per view."""
     from .schedule import heavy_first
     cam = settings.camera
     key = (tuple(np.asarray(cam.position, np.float64)), tuple(np.asarray(cam.target, np.float64)),
            tuple(np.asarray(cam.up, np.float64)), float(cam.fov_deg), tuple(settings.viewport), band_rows, rank,
-           world, str(device), None if grid is None else tuple(grid))
+           world, str(device), None if grid is None else tuple(grid), None if row_range is None else tuple(row_range))
     t = _ORDER_CACHE.get(key)
     if t is None:
         # dropping the cache is safe: cached render params own their table (render_params._keep)
         if len(_ORDER_CACHE) > 64:
             _ORDER_CACHE.clear()
-        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world, grid)).to(device)
+        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world, grid, row_range)).to(device)
         _ORDER_CACHE[key] = t
     return t

@@ -20,6 +20,10 @@ Partitioning:
   rank packs it into quads locally. Texels are independent in the reference
   build (lightbuffer.py:168-198), so the sharded build needs no halo.
 - Volume: replicated (uploaded or broadcast once per dataset).
+- Frustum-culled build (``build="frustum"``, contiguous partition,
+  partition.py): each rank renders one contiguous, cost-balanced band of
+  rows and builds only the texel-slices its band's lookups can read (K1
+  clipped by the band's two eye planes); no exchange at all.
 """
 
 from __future__ import annotations
@@ -34,6 +38,7 @@ from . import _native as N
 from .device import (DeviceVolume, current_stream_handle, device_volume, f64_tensor, pack_quads, render_params,
                      tile_order_for)
 from .lightbuffer import build_into, check_frame, lookup_reach
+from . import partition as PT
 
 
 def band_layout(height: int, band_rows: int, world: int):
@@ -109,10 +114,18 @@ class FrameRenderer:
 
     def __init__(self, volume, tf, light_cam, spec, settings, *, group=None, build: str = "replicated",
                  band_rows: int = 8, compensation_n: float = 0.0, device=None, assemble: str = "nccl",
-                 heavy_first: bool | None = None, feedback: bool | None = None, sparse: bool = True):
+                 heavy_first: bool | None = None, feedback: bool | None = None, sparse: bool = True,
+                 partition: str | None = None):
         check_frame(light_cam, spec)
-        if build not in ("replicated", "sharded"):
-            raise ValueError(f"build must be 'replicated' or 'sharded', got {build!r}")
+        if build not in ("replicated", "sharded", "frustum"):
+            raise ValueError(f"build must be 'replicated', 'sharded' or 'frustum', got {build!r}")
+        if partition is None:
+            partition = "contiguous" if build == "frustum" else "bands"
+        if partition not in ("bands", "contiguous"):
+            raise ValueError(f"partition must be 'bands' or 'contiguous', got {partition!r}")
+        if build == "frustum" and (partition != "contiguous" or not sparse):
+            raise ValueError("the frustum-culled build needs the contiguous partition and sparse K1 writes")
+        self.partition = partition
         if band_rows < 8 or band_rows % 8:
             raise ValueError("band_rows must be a positive multiple of 8")
         self.group = group
@@ -141,14 +154,11 @@ class FrameRenderer:
         self.counter = torch.zeros(1, dtype=torch.int64, device=self.dev)
         w, h = int(settings.viewport[0]), int(settings.viewport[1])
         self.width, self.height = w, h
-        self.rows_local, perm = band_layout(h, band_rows, self.world)
-        self.chunk = torch.zeros((self.rows_local, w, 4), dtype=torch.float32, device=self.dev)
-        if self.world > 1:
-            self.gathered = torch.empty((self.world * self.rows_local, w, 4), dtype=torch.float32, device=self.dev)
-            self.perm = torch.from_numpy(perm).to(self.dev)
-            self.image = torch.empty((h, w, 4), dtype=torch.float32, device=self.dev)
+        self.ranges, self.row_range, self.clip = None, None, ()
+        if partition == "contiguous":
+            self.set_ranges(PT.balanced_ranges(PT.row_costs_geometric(settings), self.world), _init=True)
         else:
-            self.image = self.chunk[:h]
+            self._layout(*band_layout(h, band_rows, self.world))
         self.set_light(light_cam, spec)
         if assemble not in ("nccl", "p2p"):
             raise ValueError(f"assemble must be 'nccl' or 'p2p', got {assemble!r}")
@@ -157,6 +167,65 @@ class FrameRenderer:
         self._parity = 0  # p2p raster buffer of the next frame
         if assemble == "p2p" and self.world > 1:
             self._setup_p2p()
+
+    # -------------------------------------------------------------- partition
+    def _layout(self, rows_local: int, perm) -> None:
+        w, h = self.width, self.height
+        self.rows_local = rows_local
+        self.chunk = torch.zeros((rows_local, w, 4), dtype=torch.float32, device=self.dev)
+        if self.world > 1:
+            self.gathered = torch.empty((self.world * rows_local, w, 4), dtype=torch.float32, device=self.dev)
+            self.perm = torch.from_numpy(perm).to(self.dev)
+            self.image = torch.empty((h, w, 4), dtype=torch.float32, device=self.dev)
+        else:
+            self.image = self.chunk[:h]
+
+    def set_ranges(self, ranges, _init: bool = False) -> None:
+        """Contiguous partition: rank r renders rows [b_r, b_r + n_r) of ``ranges``
+        (every rank passes the same list), and a frustum-culled build clips K1
+        to that band."""
+        if self.partition != "contiguous":
+            raise ValueError("row ranges need the contiguous partition")
+        ranges = [(int(b), int(n)) for b, n in ranges]
+        if len(ranges) != self.world or ranges[0][0] != 0 or sum(n for _, n in ranges) != self.height or \
+                any(n < 1 or ranges[i + 1][0] != b + n for i, (b, n) in enumerate(ranges[:-1])):
+            raise ValueError(f"ranges must tile rows 0..{self.height} with one non-empty range per rank")
+        self.ranges = ranges
+        self.row_range = ranges[self.rank]
+        rows = max(n for _, n in ranges)
+        self._layout(rows, PT.row_permutation(ranges, self.height, rows))
+        if not _init:
+            self._update_clip()
+            self._params.clear()
+            self._complete = False
+            if self.feedback is not None:
+                self.feedback.grid = None
+
+    def _update_clip(self) -> None:
+        reach = self.reach
+        if self.build_mode == "frustum" and reach is not None:
+            b, n = self.row_range
+            self.clip = PT.frustum_clip(self.settings, b, b + n, reach[0])
+        else:
+            self.clip = ()
+
+    def rebalance(self, frame_ms: float) -> list:
+        """Re-cut the contiguous bands by measured time: every rank passes the
+        device time of its last frame (build + march, CUDA events); the times
+        are exchanged (one small all-gather), spread over each band like the
+        geometric row profile, cut into balanced ranges, and each boundary
+        moves halfway there (partition.damped_ranges). Collective; returns
+        the new ranges."""
+        times = [float(frame_ms)]
+        if self.world > 1:
+            nccl = dist.get_backend(self.group) == "nccl"
+            t = torch.zeros(self.world, dtype=torch.float64, device=self.dev if nccl else "cpu")
+            t[self.rank] = float(frame_ms)
+            dist.all_reduce(t, group=self.group)
+            times = t.cpu().tolist()
+        prof = PT.calibrated_profile(PT.row_costs_geometric(self.settings), self.ranges, times)
+        self.set_ranges(PT.damped_ranges(self.ranges, PT.balanced_ranges(prof, self.world), self.height))
+        return self.ranges
 
     # -------------------------------------------------------------- p2p
     def _setup_p2p(self) -> None:
@@ -234,6 +303,7 @@ class FrameRenderer:
         if getattr(self, "_shape", None) != shape:
             self.set_light(cam, spec)
         self.cam, self.spec, self.alpha, self.offsets = cam, spec, alpha, offsets
+        self._update_clip()
         self._params.clear()
         self._complete = False
 
@@ -247,7 +317,7 @@ class FrameRenderer:
         self._shape = (n, h, w)
         self.storage = torch.empty((n, h, w, 4), dtype=torch.float32, device=self.dev)
         self.quads = self.storage
-        if self.build_mode == "replicated" or self.world == 1:
+        if self.build_mode != "sharded" or self.world == 1:
             self.shard = None
         else:
             b, e, hs = shard_rows(h, self.world, self.rank)
@@ -256,6 +326,7 @@ class FrameRenderer:
             self.plain = torch.empty((self.world * hs, n, w), dtype=torch.float32, device=self.dev)
             self.shard_rows = (b, e)
             self.shard = torch.empty((hs, n, w), dtype=torch.float32, device=self.dev)
+        self._update_clip()
         self._params.clear()
         self._complete = False
 
@@ -280,12 +351,15 @@ class FrameRenderer:
             self._complete = True
         return self.quads[..., 0]
 
+    def build_into_buffer(self, quads: torch.Tensor) -> None:
+        """This rank's K1 (replicated or frustum-culled) into ``quads``."""
+        build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, quads, self.comp, sparse=self.reach,
+                   clip=self.clip)
+
     def build(self) -> None:
         if self.shard is None:
-            reach = self.reach
-            build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, self.quads, self.comp,
-                       sparse=reach)
-            self._complete = reach is None
+            self.build_into_buffer(self.quads)
+            self._complete = self.reach is None
             return
         self._complete = True
         b, e = self.shard_rows
@@ -310,7 +384,7 @@ class FrameRenderer:
                 peer_images=self._peers[key[1]] if p2p else (),
                 heavy_first=(self.feedback is not None or self.world != 2) if self.heavy_first is None
                 else self.heavy_first,
-                lut_host=self.lut_host, feedback=self.feedback)
+                lut_host=self.lut_host, feedback=self.feedback, row_range=self.row_range)
             self._params[key] = params
         elif self.feedback is not None and self.feedback.steps is not None:
             self.feedback.steps.zero_()
@@ -392,7 +466,7 @@ class FramePipeline:
         fr = self.fr
         with torch.cuda.stream(self.build_stream):
             self.build_stream.wait_event(self.released[i])
-            build_into(fr.dvol, fr.alpha, fr.cam, fr.spec, fr.offsets, self.bufs[i], fr.comp, sparse=fr.reach)
+            fr.build_into_buffer(self.bufs[i])
             self.built[i].record(self.build_stream)
 
     def step(self, count_samples: bool = False) -> torch.Tensor:

@@ -166,14 +166,14 @@ def check_frame(cam, spec) -> None:
 
 def build_into(dvol, alpha_lut_dev, cam, spec, offsets_dev, quads: torch.Tensor, compensation_n=0.0,
                row_begin: int = 0, row_end: int | None = None, stream: int | None = None, sparse=None,
-               plain: bool = False) -> None:
+               plain: bool = False, clip=()) -> None:
     """Enqueue K1 for light rows [row_begin, row_end) into ``quads``, the
     (n, row_end - row_begin, W, 4) texel-quad view of those rows (only the
     quads within ``sparse`` reach when given)."""
     h = int(cam.resolution[1])
     row_end = h if row_end is None else row_end
     p = build_params(dvol, cam, spec, alpha_lut_dev, offsets_dev, quads, compensation_n, row_begin, row_end,
-                     sparse, plain)
+                     sparse, plain, clip)
     N.check(N.lib.sbrc_build(p, current_stream_handle() if stream is None else stream), "sbrc_build")
 
 

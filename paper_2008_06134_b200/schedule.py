@@ -20,11 +20,16 @@ from . import _native as N
 from .scene import camera_frame
 
 
-def tile_cost(settings, band_rows: int = 8, rank: int = 0, world: int = 1, grid=None) -> np.ndarray:
+def tile_cost(settings, band_rows: int = 8, rank: int = 0, world: int = 1, grid=None,
+              row_range=None) -> np.ndarray:
     """(tiles_y, tiles_x) estimated cost (mean in-cube ray length) of the rank-local K2 tiles of
-    ``grid`` (tiles_x, tiles_y, tile_w, tile_h: N.render_grid of the launch; default the block grid)."""
+    ``grid`` (tiles_x, tiles_y, tile_w, tile_h: N.render_grid of the launch; default the block grid).
+    ``row_range`` = (row_begin, row_count): a contiguous share of the rows instead of bands."""
     w, h = int(settings.viewport[0]), int(settings.viewport[1])
-    tx, ty, bw, bh = grid if grid is not None else N.march_grid(w, h, band_rows if world > 1 else 8, rank, world)
+    if grid is None:
+        grid = (N.march_grid(w, int(row_range[1]), 8, 0, 1) if row_range is not None
+                else N.march_grid(w, h, band_rows if world > 1 else 8, rank, world))
+    tx, ty, bw, bh = grid
     fr = camera_frame(settings.camera, settings.viewport)
     eye = np.asarray(settings.camera.position, dtype=np.float64)
     # sample pixels: corners and centre of every tile
@@ -32,9 +37,12 @@ def tile_cost(settings, band_rows: int = 8, rank: int = 0, world: int = 1, grid=
     gx, gy = np.meshgrid(np.arange(tx) * bw, np.arange(ty) * bh)
     px = np.clip(gx[..., None] + offs[:, 0], 0, w - 1)
     lr = gy[..., None] + offs[:, 1]
-    br = band_rows if world > 1 else 8
-    band = lr // br
-    py = np.clip((rank + band * world) * br + (lr - band * br), 0, h - 1)
+    if row_range is not None:
+        py = np.clip(int(row_range[0]) + lr, 0, h - 1)
+    else:
+        br = band_rows if world > 1 else 8
+        band = lr // br
+        py = np.clip((rank + band * world) * br + (lr - band * br), 0, h - 1)
     ndc_x = ((px + 0.5) / w * 2.0 - 1.0) * fr["tan_half"] * fr["aspect"]
     ndc_y = (1.0 - (py + 0.5) / h * 2.0) * fr["tan_half"]
     d = fr["forward"] + ndc_x[..., None] * fr["right"] + ndc_y[..., None] * fr["up2"]
@@ -52,9 +60,10 @@ def tile_cost(settings, band_rows: int = 8, rank: int = 0, world: int = 1, grid=
     return np.where(t_out > t_in, t_out - t_in, 0.0).mean(axis=-1)
 
 
-def heavy_first(settings, band_rows: int = 8, rank: int = 0, world: int = 1, grid=None) -> np.ndarray:
+def heavy_first(settings, band_rows: int = 8, rank: int = 0, world: int = 1, grid=None,
+                row_range=None) -> np.ndarray:
     """int32 dispatch table: tile indices (ty * tiles_x + tx) by decreasing cost."""
-    cost = tile_cost(settings, band_rows, rank, world, grid).reshape(-1)
+    cost = tile_cost(settings, band_rows, rank, world, grid, row_range).reshape(-1)
     return np.argsort(-cost, kind="stable").astype(np.int32)
 
 

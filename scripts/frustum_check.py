@@ -1,0 +1,102 @@
+"""Single-GPU emulation of the contiguous partition with frustum-culled builds
+(partition.py): for N = 1, 2, 4, 8 ranks of config 3, every rank's share is
+run on this GPU one after the other — its clipped K1, its march, serial and
+with the next frame's build overlapping the march — after two calibration
+frames that re-cut the bands by the measured tile costs. Each rank's rows are
+compared bit for bit with the single-GPU frame. Prints one JSON line.
+
+    python scripts/frustum_check.py [config]
+"""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_2008_06134_b200 import partition as PT  # noqa: E402
+from paper_2008_06134_b200.frame import FramePipeline, FrameRenderer  # noqa: E402
+
+
+def timed(fn, k=20):
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(k):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / k
+
+
+def rank_renderer(dvol, scene, world, rank, ranges, build="frustum"):
+    tf, cam, spec, settings = scene
+    fr = FrameRenderer(dvol, tf, cam, spec, settings, device=dvol.data.device, build=build,
+                       partition="contiguous", feedback=True)
+    fr.rank, fr.world = rank, world
+    fr.set_ranges(ranges)
+    fr.assemble = lambda: fr.chunk  # no collectives in the emulation: the rank's rows stay in its chunk
+    return fr
+
+
+def main():
+    cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    cfg = bench.CONFIGS[cfg_id]
+    dev = torch.device("cuda")
+    scene = bench.scene_objects(cfg, cfg["mode"])
+    tf, cam, spec, settings = scene
+    dvol, _ = bench.device_volume_for(cfg, dev)
+    dvol = dvol.widened()
+    ref_fr = FrameRenderer(dvol, tf, cam, spec, settings, device=dev)
+    ref = ref_fr.frame().clone()
+    full_build = timed(lambda: ref_fr.build())
+    del ref_fr
+    out = {"config": cfg_id, "full_build_ms": full_build}
+    for world in (1, 2, 4, 8):
+        shape = PT.row_costs_geometric(settings)
+        ranges = PT.balanced_ranges(shape, world)
+        history = []
+        for _ in range(6 if world > 1 else 0):  # re-cut by measured per-rank frame times
+            times = []
+            for r in range(world):
+                fr = rank_renderer(dvol, scene, world, r, ranges)
+                times.append(timed(lambda: (fr.build(), fr.march(False)), k=5))
+                del fr
+            history.append({"ranges": ranges, "max_ms": max(times), "times": times})
+            ranges = PT.damped_ranges(ranges, PT.balanced_ranges(PT.calibrated_profile(shape, ranges, times), world),
+                                      settings.viewport[1])
+        if history:  # the best cut seen
+            ranges = min(history, key=lambda e: e["max_ms"])["ranges"]
+        ranks = []
+        same = True
+        for r in range(world):
+            fr = rank_renderer(dvol, scene, world, r, ranges)
+            b, n = fr.row_range
+            fr.build()
+            fr.march(False)
+            same &= bool(torch.equal(fr.chunk[:n], ref[b:b + n]))
+            t_build = timed(fr.build)
+            t_march = timed(lambda: fr.march(False))
+            t_serial = timed(lambda: (fr.build(), fr.march(False)))
+            pipe = FramePipeline(fr)
+            t_pipe = timed(lambda: pipe.step())
+            pipe.drain()
+            torch.cuda.synchronize()
+            same &= bool(torch.equal(fr.chunk[:n], ref[b:b + n]))
+            ranks.append({"rows": [b, n], "build_ms": t_build, "march_ms": t_march, "serial_ms": t_serial,
+                          "pipelined_ms": t_pipe})
+            del pipe, fr
+            torch.cuda.empty_cache()
+        out[world] = {"ranges": ranges, "identical": same, "calibration": history,
+                      "max_build_ms": max(x["build_ms"] for x in ranks),
+                      "max_march_ms": max(x["march_ms"] for x in ranks),
+                      "max_serial_ms": max(x["serial_ms"] for x in ranks),
+                      "max_pipelined_ms": max(x["pipelined_ms"] for x in ranks), "ranks": ranks}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
