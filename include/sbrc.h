@@ -234,6 +234,20 @@ int sbrc_volume_check(const sbrc_volume* v);
  * numpy's float32 arithmetic, so bit-identical. */
 int sbrc_normalize_f32(float* data, int64_t n, float lo, float range, void* stream);
 
+/* K0: widen a raw u8/u16 voxel stream (n voxels, voxel_type SBRC_VOXEL_U8 /
+ * U16) to float32 with load_raw's normalisation (volume.py:143-146: IEEE
+ * float32 division by 255 / 65535, bit-identical to numpy). */
+int sbrc_widen_volume(const void* src, int voxel_type, int64_t n, float* dst, void* stream);
+
+/* Heavy-first dispatch table from measured tile costs (schedule.TileFeedback):
+ * order[0..n) = tile indices by decreasing steps[i], ties by increasing index
+ * (deterministic). Device pointers; replaces a stable descending argsort. */
+int sbrc_tile_order(const unsigned int* steps, int n, int* order, void* stream);
+
+/* Image assembly of the NCCL path: dst row y (width float4 pixels) = src row
+ * perm[y], y < rows (device pointers; perm int64). */
+int sbrc_permute_rows(const float* src, const int64_t* perm, float* dst, int rows, int width, void* stream);
+
 /* K1: attenuation build (lightbuffer.py:144-199). */
 int sbrc_build(const sbrc_build_params* p, void* stream);
 

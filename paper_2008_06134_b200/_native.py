@@ -32,7 +32,8 @@ EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume
            "sbrc_build", "sbrc_render", "sbrc_pack_quads", "sbrc_shadow_oracle", "sbrc_light_factor",
            "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_ipc_alloc", "sbrc_ipc_free", "sbrc_ipc_handle",
            "sbrc_ipc_open", "sbrc_ipc_close", "sbrc_march_grid", "sbrc_local_rows",
-           "sbrc_render_grid", "sbrc_host_device_pointer", "sbrc_debug_violations")
+           "sbrc_render_grid", "sbrc_host_device_pointer", "sbrc_debug_violations", "sbrc_widen_volume",
+           "sbrc_tile_order", "sbrc_permute_rows")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -119,6 +120,9 @@ def _load() -> C.CDLL:
                                     C.POINTER(C.c_int), C.c_void_p]
     lib.sbrc_debug_violations.argtypes = [C.POINTER(C.c_uint * 8), C.c_int]
     lib.sbrc_normalize_f32.argtypes = [C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_void_p]
+    lib.sbrc_widen_volume.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
+    lib.sbrc_tile_order.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    lib.sbrc_permute_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
     lib.sbrc_shadow_oracle.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_double, C.c_void_p, C.c_void_p]
     lib.sbrc_pack_quads.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,

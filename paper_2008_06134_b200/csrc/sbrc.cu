@@ -463,6 +463,68 @@ __global__ void __launch_bounds__(256) normalize_f32_kernel(float* data, long lo
     data[i] = __fdiv_rn(__fsub_rn(data[i], lo), range);
 }
 
+// K0 widening: a raw u8/u16 volume to float32 with load_raw's IEEE float32
+// division (volume.py:143-146: astype(float32) / 255.0 or / 65535.0, the
+// Python divisor a float32 under NEP 50) in one pass; the integers convert
+// exactly. Vectorised: 4 voxels per thread per step.
+template <typename T>
+__global__ void __launch_bounds__(256) widen_kernel(const T* __restrict__ src, float* __restrict__ dst, long long n,
+                                                   float scale) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long n4 = n / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    T v[4];
+    if constexpr (sizeof(T) == 1) {
+      const uchar4 q = reinterpret_cast<const uchar4*>(src)[i];
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const ushort4 q = reinterpret_cast<const ushort4*>(src)[i];
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    }
+    reinterpret_cast<float4*>(dst)[i] = make_float4(__fdiv_rn((float)v[0], scale), __fdiv_rn((float)v[1], scale),
+                                                    __fdiv_rn((float)v[2], scale), __fdiv_rn((float)v[3], scale));
+  }
+  for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = __fdiv_rn((float)src[i], scale);
+}
+
+// Heavy-first order from measured tile costs (schedule.TileFeedback): tiles
+// by decreasing steps, ties by increasing index — every key
+// (~steps << 32 | index) is unique, so its rank among all keys is its slot
+// and the order is deterministic. Rank by counting: each thread owns one key
+// and compares it with all n keys, staged through shared memory 256 at a
+// time (O(n^2) compares; 16K tiles take ~15 us on 148 SMs, no sort library).
+__global__ void __launch_bounds__(256) rank_order_kernel(const unsigned* __restrict__ steps, int n,
+                                                         int* __restrict__ order) {
+  __shared__ unsigned long long tile[256];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long mine =
+      i < n ? ((unsigned long long)(~__ldg(steps + i)) << 32) | (unsigned)i : ~0ull;
+  int rank = 0;
+  for (int base = 0; base < n; base += 256) {
+    const int j = base + threadIdx.x;
+    tile[threadIdx.x] = j < n ? ((unsigned long long)(~__ldg(steps + j)) << 32) | (unsigned)j : ~0ull;
+    __syncthreads();
+    const int m = min(256, n - base);
+#pragma unroll 8
+    for (int k = 0; k < m; ++k) rank += tile[k] < mine;
+    __syncthreads();
+  }
+  if (i < n) order[rank] = i;
+}
+
+// Image assembly of the NCCL path: raster row y = gathered row perm[y]
+// (float4 pixels, one warp-strided row copy per block row).
+__global__ void __launch_bounds__(256) permute_rows_kernel(const float4* __restrict__ src,
+                                                           const long long* __restrict__ perm, float4* __restrict__ dst,
+                                                           int rows, int width) {
+  for (int y = blockIdx.x; y < rows; y += gridDim.x) {
+    const float4* s = src + (size_t)__ldg(perm + y) * width;
+    float4* d = dst + (size_t)y * width;
+    for (int x = threadIdx.x; x < width; x += blockDim.x) d[x] = __ldg(s + x);
+  }
+}
+
 // ---------------------------------------------------------------- half-angle baseline
 // halfangle.py:48-142. Float64 throughout, reference op order for the slice
 // geometry; alpha correction a = 1 - (1 - alpha)^exponent via pow.
@@ -744,6 +806,34 @@ int sbrc_normalize_f32(float* data, int64_t n, float lo, float range, void* stre
   if (data == nullptr || n < 0 || !(range > 0.0f)) return SBRC_EINVAL;
   if (n == 0) return SBRC_OK;
   normalize_f32_kernel<<<148 * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(data, n, lo, range);
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_widen_volume(const void* src, int voxel_type, int64_t n, float* dst, void* stream) {
+  if (src == nullptr || dst == nullptr || n < 0) return SBRC_EINVAL;
+  if (voxel_type != SBRC_VOXEL_U8 && voxel_type != SBRC_VOXEL_U16) return SBRC_EINVAL;
+  if (n == 0) return SBRC_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (voxel_type == SBRC_VOXEL_U8)
+    widen_kernel<unsigned char><<<148 * 8, 256, 0, s>>>(static_cast<const unsigned char*>(src), dst, n, 255.0f);
+  else
+    widen_kernel<unsigned short><<<148 * 8, 256, 0, s>>>(static_cast<const unsigned short*>(src), dst, n, 65535.0f);
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_tile_order(const unsigned int* steps, int n, int* order, void* stream) {
+  if (steps == nullptr || order == nullptr || n < 0) return SBRC_EINVAL;
+  if (n == 0) return SBRC_OK;
+  rank_order_kernel<<<(n + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(steps, n, order);
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_permute_rows(const float* src, const int64_t* perm, float* dst, int rows, int width, void* stream) {
+  if (src == nullptr || perm == nullptr || dst == nullptr || rows < 0 || width < 1) return SBRC_EINVAL;
+  if (rows == 0) return SBRC_OK;
+  permute_rows_kernel<<<min(rows, 148 * 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4*>(src), reinterpret_cast<const long long*>(perm), reinterpret_cast<float4*>(dst),
+      rows, width);
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 

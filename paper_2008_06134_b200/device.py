@@ -74,13 +74,10 @@ class DeviceVolume:
         compute at fetch, so results are identical."""
         if self.voxel_type == N.VOXEL_F32:
             return self
-        raw = self.data.to(torch.int32)
-        if self.voxel_type == N.VOXEL_U16:
-            raw = raw & 0xFFFF
-        f = raw.to(torch.float32)  # exact for integers < 2^24
-        scale = 255.0 if self.voxel_type == N.VOXEL_U8 else 65535.0
-        N.check(N.lib.sbrc_normalize_f32(f.data_ptr(), f.numel(), 0.0, scale, current_stream_handle()),
-                "sbrc_normalize_f32")
+        f = torch.empty(self.data.numel(), dtype=torch.float32, device=self.data.device)
+        N.check(N.lib.sbrc_widen_volume(self.data.data_ptr(), self.voxel_type, f.numel(), f.data_ptr(),
+                                        current_stream_handle()), "sbrc_widen_volume")
+        f = f.view(self.data.shape)
         out = DeviceVolume(f, N.VOXEL_F32, self.dims, self.box_lo, self.box_hi, source_type=self.voxel_type)
         out._value_min = self._value_min
         return out

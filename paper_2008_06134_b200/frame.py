@@ -407,7 +407,11 @@ class FrameRenderer:
                 self._parity ^= 1
                 return out
             all_gather_into(self.gathered, self.chunk, self.group)
-            torch.index_select(self.gathered, 0, self.perm, out=self.image)
+            if self.gathered.is_cuda:
+                N.check(N.lib.sbrc_permute_rows(self.gathered.data_ptr(), self.perm.data_ptr(), self.image.data_ptr(),
+                                                self.height, self.width, current_stream_handle()), "sbrc_permute_rows")
+            else:
+                torch.index_select(self.gathered, 0, self.perm, out=self.image)
         return self.image
 
     def close(self) -> None:

@@ -93,5 +93,10 @@ class TileFeedback:
     def update(self) -> None:
         """Sort the tiles just measured (call after the launch, same stream)."""
         if self.steps is not None:
-            idx = torch.argsort(self.steps, descending=True, stable=True)
-            self.order.copy_(idx.to(torch.int32))
+            if self.steps.is_cuda:  # sbrc_tile_order: rank-by-count kernel on the launching stream
+                from .device import current_stream_handle
+                N.check(N.lib.sbrc_tile_order(self.steps.data_ptr(), self.steps.numel(), self.order.data_ptr(),
+                                              current_stream_handle()), "sbrc_tile_order")
+            else:  # host tensors (CPU tests of the ordering rule)
+                idx = torch.argsort(self.steps, descending=True, stable=True)
+                self.order.copy_(idx.to(torch.int32))

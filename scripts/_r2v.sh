@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -s -p no:cacheprovider > gpurun_out/r2v_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r2v_pytest.log

@@ -1,0 +1,60 @@
+"""The small native kernels around the path (no eager PyTorch on the
+per-frame path): K0 widening, the measured heavy-first order, the NCCL
+assembly's row permutation. Needs a B200."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+    return torch
+
+
+def test_widen_volume_every_value(torch):
+    """sbrc_widen_volume equals numpy's float32 load_raw normalisation
+    (volume.py:143-146) for every u8 and u16 value, ragged lengths included."""
+    from paper_2008_06134_b200 import _native as N
+    from paper_2008_06134_b200.device import current_stream_handle
+    for vt, dt, scale in ((N.VOXEL_U8, np.uint8, 255.0), (N.VOXEL_U16, np.uint16, 65535.0)):
+        vals = np.arange(np.iinfo(dt).max + 1, dtype=dt)
+        for n in (len(vals), len(vals) - 3):
+            host = vals[:n]
+            src = torch.from_numpy(host.view(np.int8 if dt == np.uint8 else np.int16).copy()).cuda()
+            out = torch.empty(n, dtype=torch.float32, device="cuda")
+            N.check(N.lib.sbrc_widen_volume(src.data_ptr(), vt, n, out.data_ptr(), current_stream_handle()), "widen")
+            want = host.astype(np.float32) / np.float32(scale)
+            assert np.array_equal(out.cpu().numpy(), want), (vt, n)
+
+
+def test_tile_order_matches_stable_argsort(torch):
+    from paper_2008_06134_b200 import _native as N
+    from paper_2008_06134_b200.device import current_stream_handle
+    rng = np.random.default_rng(3)
+    for n in (1, 7, 256, 257, 5000, 16384):
+        steps = torch.from_numpy(rng.integers(0, 40, n).astype(np.int32)).cuda()  # many ties
+        order = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+        N.check(N.lib.sbrc_tile_order(steps.data_ptr(), n, order.data_ptr(), current_stream_handle()), "order")
+        want = torch.argsort(steps, descending=True, stable=True).to(torch.int32)
+        assert torch.equal(order, want), n
+
+
+def test_permute_rows_matches_index_select(torch):
+    from paper_2008_06134_b200 import _native as N
+    from paper_2008_06134_b200.device import current_stream_handle
+    from paper_2008_06134_b200.frame import band_layout
+    h, w = 1031, 37
+    rows, perm = band_layout(h, 16, 3)
+    src = torch.randn((3 * rows, w, 4), device="cuda")
+    p = torch.from_numpy(perm).cuda()
+    dst = torch.empty((h, w, 4), device="cuda")
+    N.check(N.lib.sbrc_permute_rows(src.data_ptr(), p.data_ptr(), dst.data_ptr(), h, w, current_stream_handle()),
+            "permute")
+    assert torch.equal(dst, torch.index_select(src, 0, p))
