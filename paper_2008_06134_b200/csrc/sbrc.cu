@@ -5,6 +5,11 @@
 
 #include "sbrc_common.cuh"
 
+#include <cudaTypedefs.h>  // CUtensorMap, PFN_cuTensorMapEncodeTiled (driver entry point; no libcuda link)
+
+#include <climits>
+#include <cmath>
+
 namespace {
 
 // ---------------------------------------------------------------- K1 build
@@ -44,10 +49,54 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// TMA-staged volume tiles (D = -1, float32 volumes in the unit box): the
+// block's texel-slice points of C consecutive slices lie in a small
+// parallelepiped of the volume; its axis-aligned bounding box is loaded into
+// shared memory by one cp.async.bulk.tensor.3d (TMA, mbarrier completion),
+// double-buffered so the box of the next C slices streams in while this one
+// is sampled, and the 8 corner gathers of each point become shared-memory
+// loads. Box shape and C come from the light geometry (tma_plan).
+#ifndef SBRC_BUILD_TMA
+#define SBRC_BUILD_TMA 0  // A/B option: bit-exact but 3.3x slower on config 3 (profiles/r2_notes.md)
+#endif
+#ifndef SBRC_BUILD_TMA_SMEM
+#define SBRC_BUILD_TMA_SMEM (100 * 1024)  // shared-memory budget of the two boxes per block
+#endif
+#ifndef SBRC_BUILD_TMA_MINB
+#define SBRC_BUILD_TMA_MINB 2
+#endif
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(m))
+      : "memory");
+}
+
 template <int VT, bool UNIT, int D>
-__global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, D > 0 ? SBRC_BUILD_ASYNC_MINB : SBRC_BUILD_MINB)
-    build_kernel(const sbrc_build_params P) {
-  static_assert(D == 0 || VT == SBRC_VOXEL_F32, "the async gather pipeline copies 4-byte voxels");
+__global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS,
+                                  D > 0 ? SBRC_BUILD_ASYNC_MINB : (D < 0 ? SBRC_BUILD_TMA_MINB : SBRC_BUILD_MINB))
+    build_kernel(const sbrc_build_params P, const __grid_constant__ CUtensorMap tmap, const int4 tbox) {
+  static_assert(D == 0 || VT == SBRC_VOXEL_F32, "the async gather / TMA pipelines copy 4-byte voxels");
+  static_assert(D >= 0 || UNIT, "TMA boxes are placed in unit-box voxel coordinates");
   __shared__ double lut[SBRC_LUT_SIZE];
   __shared__ double u8tab[VT == SBRC_VOXEL_U8 ? 256 : 1];
   for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < SBRC_LUT_SIZE; i += blockDim.x * blockDim.y)
@@ -62,8 +111,11 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, D > 0 ? SBRC_BUILD_ASYNC
   const int lane = threadIdx.x;
   const int x = blockIdx.x * 31 + lane;
   const int y = P.row_begin + blockIdx.y * blockDim.y + threadIdx.y;
-  if (y >= P.row_end) return;  // whole warp (warps are rows)
-  const bool owner = lane < 31 && x < L.width;
+  const bool row_ok = y < P.row_end;
+  if constexpr (D >= 0) {
+    if (!row_ok) return;  // whole warp (warps are rows)
+  }
+  const bool owner = row_ok && lane < 31 && x < L.width;
 
   // Texel centre in world (u, v) plane coordinates (_texel_world_grid, :134-141):
   // u0 + (i + 0.5) / W * (u1 - u0).
@@ -186,6 +238,10 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, D > 0 ? SBRC_BUILD_ASYNC
     }
   }
   auto writes = [&](int kk) { return owner && kk >= w_lo && kk <= w_hi; };
+  if (!row_ok) {  // (TMA blocks only: rows past the end idle through the block's barriers)
+    k_lo = n;
+    k_hi = -1;
+  }
   const int kA = __reduce_min_sync(0xffffffffu, k_lo <= k_hi ? k_lo : n);
   int kB = __reduce_max_sync(0xffffffffu, k_lo <= k_hi ? k_hi : -1);
   if (P.write_sparse && P.n_clip > 0) {
@@ -199,7 +255,9 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, D > 0 ? SBRC_BUILD_ASYNC
   const int pre_end = kA > kB ? n : kA - 1;  // quads 0 .. kA-2 hold layers < kA only
   if (owner)
     for (int kk = max(0, w_lo), e = min(pre_end, w_hi + 1); kk < e; ++kk) put(kk, ones);
-  if (kA > kB) return;
+  if constexpr (D >= 0) {
+    if (kA > kB) return;
+  }
   auto emit_w = [&](int kk, float a, float b) {  // all lanes shuffle; stores only where written
     float ra = __shfl_down_sync(0xffffffffu, a, 1), rb = __shfl_down_sync(0xffffffffu, b, 1);
     if (x == L.width - 1) {
@@ -210,7 +268,123 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS, D > 0 ? SBRC_BUILD_ASYNC
   };
   prev = 1.0f;
   int k = kA;
-  if constexpr (D > 0) {
+  if constexpr (D < 0) {
+    extern __shared__ unsigned char tma_smem[];
+    __shared__ int kblk[2];
+    __shared__ int orig[2][3];
+    __shared__ __align__(8) unsigned long long mbar[2];
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int bx = tbox.x, by = tbox.y, bz = tbox.z, C = tbox.w;
+    const int bxy = bx * by, box_n = bxy * bz;
+    const unsigned box_bytes = (unsigned)box_n * 4u;
+    float* bufs[2];
+    bufs[0] = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tma_smem) + 127) & ~(uintptr_t)127);
+    bufs[1] = bufs[0] + ((box_n + 31) & ~31);  // 128-byte aligned
+    if (tid == 0) {
+      kblk[0] = n;
+      kblk[1] = -1;
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (lane == 0 && kA <= kB) {
+      atomicMin(&kblk[0], kA);
+      atomicMax(&kblk[1], kB);
+    }
+    __syncthreads();
+    const int KA = kblk[0], KB = kblk[1];
+    const int nch = KA > KB ? 0 : (KB - KA) / C + 1;
+    const int dims[3] = {P.volume.nx, P.volume.ny, P.volume.nz};
+    const unsigned nx = (unsigned)dims[0];
+    // the block's corner texels (lanes 0..31 of rows row0 .. row0+3, clipped)
+    const int xb[2] = {(int)blockIdx.x * 31, min((int)blockIdx.x * 31 + 31, L.width - 1)};
+    const int yb0 = P.row_begin + (int)(blockIdx.y * blockDim.y);
+    const int yb[2] = {yb0, min(yb0 + (int)blockDim.y - 1, P.row_end - 1)};
+    // chunk i: slices [KA + i C, KA + i C + C - 1]; box origin = min over the 8
+    // corners of the parallelepiped of floor(g) (the positions are affine in
+    // texel and slice index), less one voxel of margin for float64 rounding
+    auto issue = [&](int i) {
+      const int c0 = KA + i * C, c1 = min(c0 + C - 1, KB);
+      int mn[3] = {INT_MAX, INT_MAX, INT_MAX};
+#pragma unroll 1
+      for (int j = 0; j < 8; ++j) {
+        const int xx = xb[j & 1], yy = yb[(j >> 1) & 1], kk = (j & 4) ? c1 : c0;
+        const double u = dadd(L.u_range[0], dmul(ddiv(dadd((double)xx, 0.5), (double)L.width),
+                                                 dsub(L.u_range[1], L.u_range[0])));
+        const double v = dadd(L.v_range[0], dmul(ddiv(dadd((double)yy, 0.5), (double)L.height),
+                                                 dsub(L.v_range[1], L.v_range[0])));
+        const double off = __ldg(L.plane_offsets + kk);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double pc = dadd(dadd(dmul(u, L.axis_u[c]), dmul(v, L.axis_v[c])), dmul(off, L.light_dir[c]));
+          mn[c] = min(mn[c], (int)floor(pc * dims[c] - 0.5));
+        }
+      }
+      const int b = i & 1;
+      const int bx0 = (mn[0] - 1) & ~3;  // the box's first x must be 16-byte aligned (TMA faults otherwise)
+      orig[b][0] = bx0;
+      orig[b][1] = mn[1] - 1;
+      orig[b][2] = mn[2] - 1;
+      mbar_expect_tx(&mbar[b], box_bytes);
+      tma_load_3d(bufs[b], &tmap, bx0, mn[1] - 1, mn[2] - 1, &mbar[b]);
+    };
+    if (tid == 0 && nch > 0) issue(0);
+    for (int i = 0; i < nch; ++i) {
+      if (tid == 0 && i + 1 < nch) {
+        // buffer (i+1)&1 was last read in chunk i-1, before the barrier that ended it
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(i + 1);
+      }
+      const int b = i & 1;
+      mbar_wait(&mbar[b], (unsigned)((i >> 1) & 1));
+      const float* sb = bufs[b];
+      const int ox = orig[b][0], oy = orig[b][1], oz = orig[b][2];
+      const int c0 = KA + i * C;
+      const int k0 = max(c0, kA), k1 = min(c0 + C - 1, kB);  // this warp's slices of the chunk
+      for (int kk = k0; kk <= k1; ++kk) {
+        double p[3];
+        point(kk, p[0], p[1], p[2]);
+        const bool cov = in_cube(p[0], p[1], p[2]);
+        Cell<VT> cl;
+        if (cov) {
+          int lo[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {  // cell_fetch's arithmetic (volume.py:175-182), unit box
+            const double g = dsub(dmul(p[c], (double)dims[c]), 0.5);
+            const FloorD fl = floor_d(g);
+            cl.f[c] = dsub(g, fl.f);
+            lo[c] = fl.i;
+          }
+          if ((unsigned)lo[0] < nx - 1 && (unsigned)lo[1] < (unsigned)(dims[1] - 1) &&
+              (unsigned)lo[2] < (unsigned)(dims[2] - 1)) {
+            const int o = ((lo[2] - oz) * by + (lo[1] - oy)) * bx + (lo[0] - ox);
+            SBRC_CHECK(o >= 0 && o + bxy + bx + 1 < box_n, 0);
+            cl.r[0] = sb[o]; cl.r[1] = sb[o + 1]; cl.r[2] = sb[o + bx]; cl.r[3] = sb[o + bx + 1];
+            cl.r[4] = sb[o + bxy]; cl.r[5] = sb[o + bxy + 1]; cl.r[6] = sb[o + bxy + bx]; cl.r[7] = sb[o + bxy + bx + 1];
+          } else {
+            int a3[3], b3[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              a3[c] = min(max(lo[c], 0), dims[c] - 1);
+              b3[c] = min(max(lo[c] + 1, 0), dims[c] - 1);
+            }
+            const int z0 = (a3[2] - oz) * bxy, z1 = (b3[2] - oz) * bxy, y0 = (a3[1] - oy) * bx, y1 = (b3[1] - oy) * bx;
+            const int x0 = a3[0] - ox, x1 = b3[0] - ox;
+            SBRC_CHECK(z0 + y0 + x0 >= 0 && z1 + y1 + x1 < box_n, 0);
+            cl.r[0] = sb[z0 + y0 + x0]; cl.r[1] = sb[z0 + y0 + x1]; cl.r[2] = sb[z0 + y1 + x0]; cl.r[3] = sb[z0 + y1 + x1];
+            cl.r[4] = sb[z1 + y0 + x0]; cl.r[5] = sb[z1 + y0 + x1]; cl.r[6] = sb[z1 + y1 + x0]; cl.r[7] = sb[z1 + y1 + x1];
+          }
+        }
+        const float st = step_slice(cov, cl);
+        if (kk > 0) emit_w(kk - 1, prev, st);
+        prev = st;
+      }
+      __syncthreads();
+    }
+    if (kA > kB) return;
+    k = kB + 1;
+  } else if constexpr (D > 0) {
     // Stage st of this thread: corner voxels svox[st][c][tid] (landed by
     // cp.async) and the cell fractions sfr[st][a][tid] (float64, stored at
     // issue; sfr[st][0] = -1 marks an uncovered texel-slice point). Each
@@ -645,13 +819,84 @@ void has_passes(const sbrc_half_angle_params& p, int k0, int k1, cudaStream_t s)
   }
 }
 
+// cuTensorMapEncodeTiled from the driver through the runtime (resolved once;
+// the library links only cudart).
+static PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
+  static const PFN_cuTensorMapEncodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (PFN_cuTensorMapEncodeTiled) nullptr;
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(f);
+  }();
+  return fn;
+}
+
+// TMA plan of a build: the box (voxels) covering one block's texel-slice
+// points over C slices plus the cell corners and a rounding margin, the
+// largest C whose two boxes fit SBRC_BUILD_TMA_SMEM. False when the volume
+// or geometry does not suit TMA (row pitch not a multiple of 16 bytes, box
+// dims > 256, unaligned base): the register path is used.
+static bool tma_plan(const sbrc_build_params& p, int4* box, size_t* smem) {
+  const sbrc_volume& v = p.volume;
+  const sbrc_light_frame& L = p.light;
+  if ((v.nx % 4) != 0 || (reinterpret_cast<uintptr_t>(v.data) % 16) != 0) return false;
+  const double du = (L.u_range[1] - L.u_range[0]) / L.width, dv = (L.v_range[1] - L.v_range[0]) / L.height;
+  const double dk = (L.d_max - L.d_min) / L.n_slices;
+  const int dims[3] = {v.nx, v.ny, v.nz};
+  for (int C = 8; C >= 1; --C) {
+    int b[3];
+    bool ok = true;
+    for (int c = 0; c < 3; ++c) {
+      const double ext = (fabs(L.axis_u[c]) * 31.0 * du + fabs(L.axis_v[c]) * (SBRC_BUILD_ROWS - 1) * dv +
+                          fabs(L.light_dir[c]) * (C - 1) * dk) * dims[c];
+      b[c] = (int)ceil(ext) + 4;
+      if (b[c] > 256) ok = false;
+    }
+    b[0] = (b[0] + 3 + 3) & ~3;  // 16-byte rows; +3: the origin x is rounded down to a multiple of 4
+    if (!ok || b[0] > 256) continue;
+    const size_t box_n = (size_t)b[0] * b[1] * b[2];
+    const size_t bytes = 2 * (((box_n + 31) & ~(size_t)31) * 4) + 128;
+    if (bytes > SBRC_BUILD_TMA_SMEM) continue;
+    *box = make_int4(b[0], b[1], b[2], C);
+    *smem = bytes;
+    return true;
+  }
+  return false;
+}
+
 template <int VT>
 void launch_build(const sbrc_build_params& p, cudaStream_t s) {
   dim3 block(32, SBRC_BUILD_ROWS);  // warps are rows of 31 owned texels (build_kernel)
   dim3 grid((p.light.width + 30) / 31, (p.row_end - p.row_begin + SBRC_BUILD_ROWS - 1) / SBRC_BUILD_ROWS);
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  const int4 none = make_int4(0, 0, 0, 0);
+  if constexpr (VT == SBRC_VOXEL_F32) {
+    int4 box;
+    size_t smem;
+    PFN_cuTensorMapEncodeTiled enc = SBRC_BUILD_TMA ? tensor_map_encoder() : nullptr;
+    if (enc != nullptr && unit_box(p.volume) && tma_plan(p, &box, &smem)) {
+      const cuuint64_t gdim[3] = {(cuuint64_t)p.volume.nx, (cuuint64_t)p.volume.ny, (cuuint64_t)p.volume.nz};
+      const cuuint64_t gstride[2] = {(cuuint64_t)p.volume.nx * 4, (cuuint64_t)p.volume.nx * p.volume.ny * 4};
+      const cuuint32_t bdim[3] = {(cuuint32_t)box.x, (cuuint32_t)box.y, (cuuint32_t)box.z};
+      const cuuint32_t estride[3] = {1, 1, 1};
+      if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(p.volume.data), gdim, gstride, bdim,
+              estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+        auto kern = build_kernel<VT, true, -1>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, block, smem, s>>>(p, tmap, box);
+        return;
+      }
+    }
+  }
   constexpr int D = VT == SBRC_VOXEL_F32 ? SBRC_BUILD_ASYNC : 0;
-  if (unit_box(p.volume)) build_kernel<VT, true, D><<<grid, block, 0, s>>>(p);
-  else build_kernel<VT, false, D><<<grid, block, 0, s>>>(p);
+  if (unit_box(p.volume)) build_kernel<VT, true, D><<<grid, block, 0, s>>>(p, tmap, none);
+  else build_kernel<VT, false, D><<<grid, block, 0, s>>>(p, tmap, none);
 }
 
 }  // namespace

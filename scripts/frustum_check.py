@@ -7,6 +7,7 @@ compared bit for bit with the single-GPU frame. Prints one JSON line.
 
     python scripts/frustum_check.py [config]
 """
+import gc
 import json
 import sys
 
@@ -65,6 +66,7 @@ def main():
                 fr = rank_renderer(dvol, scene, world, r, ranges)
                 times.append(timed(lambda: (fr.build(), fr.march(False)), k=5))
                 del fr
+                gc.collect()
             history.append({"ranges": ranges, "max_ms": max(times), "times": times})
             ranges = PT.damped_ranges(ranges, PT.balanced_ranges(PT.calibrated_profile(shape, ranges, times), world),
                                       settings.viewport[1])
@@ -89,6 +91,7 @@ def main():
             ranks.append({"rows": [b, n], "build_ms": t_build, "march_ms": t_march, "serial_ms": t_serial,
                           "pipelined_ms": t_pipe})
             del pipe, fr
+            gc.collect()
             torch.cuda.empty_cache()
         out[world] = {"ranges": ranges, "identical": same, "calibration": history,
                       "max_build_ms": max(x["build_ms"] for x in ranks),
