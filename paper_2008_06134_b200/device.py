@@ -167,7 +167,10 @@ def f64_tensor(arr, device) -> torch.Tensor:
     """float64 host array -> device, staged through pinned memory and copied
     asynchronously on the current stream (the pinned block is recycled by
     torch's caching host allocator once the copy has completed)."""
-    host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    if not a.flags.writeable:  # read-only cached arrays (scene.camera_frame): torch wants a writable buffer
+        a = a.copy()
+    host = torch.from_numpy(a)
     return host.pin_memory().to(device, non_blocking=True)
 
 
