@@ -4,8 +4,11 @@
     SBRC_LIB=$PWD/paper_2008_06134_b200/_sbrc_checked.so python scripts/checked_run.py
 
 Runs scripts/sanitize_run.py's workload (every kernel, every mode, ray
-groups, peer-raster stores, sparse/plain builds) plus a config-3 frame on
-the checked library and prints the violation counters by kind; all must be 0.
+groups, peer-raster stores, sparse/plain builds) plus config-2/3 frames, the
+8 contiguous ranks of config 3 with frustum-culled builds, on the checked
+library and prints the violation counters by kind; all must be 0. Built
+with -DSBRC_BUILD_TMA=1 too, the TMA-staged K1's shared-memory box reads
+are checked as well (kind "volume").
 """
 import ctypes as C
 import json
@@ -37,6 +40,18 @@ def main():
         fr = FrameRenderer(dvol, tf, cam, spec, settings)
         fr.frame()
         fr.intensity  # full build too
+    from paper_2008_06134_b200 import partition as PT
+    cfg = bench.CONFIGS[3]
+    tf, cam, spec, settings = bench.scene_objects(cfg, cfg["mode"])
+    dvol, _ = bench.device_volume_for(cfg, torch.device("cuda"))
+    ranges = PT.balanced_ranges(PT.row_costs_geometric(settings), 8)
+    for r in range(8):  # contiguous bands, clipped K1 + row-range K2
+        fr = FrameRenderer(dvol, tf, cam, spec, settings, build="frustum")
+        fr.rank, fr.world = r, 8
+        fr.set_ranges(ranges)
+        fr.build()
+        fr.march()
+        del fr
     torch.cuda.synchronize()
     N.check(N.lib.sbrc_debug_violations(C.byref(counts), 0), "sbrc_debug_violations")
     out = dict(zip(KINDS, list(counts)))

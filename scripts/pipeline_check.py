@@ -1,5 +1,6 @@
 """Single-GPU check of frame pipelining: serial (build; march) vs pipelined,
 for the full frame (N=1) and for one rank's share at N=8 (rank 0 of 8)."""
+import gc
 import json
 import sys
 
@@ -41,10 +42,11 @@ def timed(fn, k=20):
 
 
 def main():
-    cfg = bench.CONFIGS[3]
+    cfg = bench.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 3]
     dev = torch.device("cuda")
-    tf, cam, spec, settings = bench.scene_objects(cfg, "cone")
+    tf, cam, spec, settings = bench.scene_objects(cfg, cfg["mode"])
     dvol, _ = bench.device_volume_for(cfg, dev)
+    dvol = dvol.widened()
     out = {}
     for world in (1, 2, 4, 8):
         fr = FakeRank(dvol, tf, cam, spec, settings, device=dev, rank=0, world=world, feedback=world > 1)
@@ -62,6 +64,9 @@ def main():
         same = bool(torch.equal(pipe2.fr.chunk, ref))
         out[world] = {"serial_ms": serial, "pipelined_ms": piped, "pipelined_drain_each_ms": piped_drain,
                       "identical": same}
+        del fr, pipe, pipe2, ref
+        gc.collect()
+        torch.cuda.empty_cache()
     print(json.dumps(out))
 
 
