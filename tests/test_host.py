@@ -223,3 +223,28 @@ def test_tile_feedback_order():
     assert order2 is fb.order and int(steps2.sum()) == 0          # same grid: order kept, costs zeroed
     order3, _ = fb.prepare((2, 2, 32, 8), torch.arange(4, dtype=torch.int32))
     assert order3.tolist() == [0, 1, 2, 3]                          # new grid: fresh initial order
+
+
+@pytest.mark.parametrize("light,res,n", [((0.3, -0.5, 0.8), 48, 24), ((0.0, 0.0, 1.0), 16, 8), ((1.0, 1.0, 1.0), 33, 17)])
+def test_covered_texel_slices_matches_brute_force(light, res, n):
+    """bench.covered_texel_slices (the K1 algorithmic-byte count: an analytic
+    slab count per texel line) matches the number of texel-slice points the
+    oracle's build tests as inside the cube (lightbuffer.py:182-183) to 0.5%
+    (points within rounding of a cube face may go either way)."""
+    import sys
+    from conftest import ROOT
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2008_06134_b200 import scene
+    cam = scene.LightCamera.fit(light, (1, 1, 1), (res, res))
+    spec = scene.make_slice_stack(light, n)
+    w, h = cam.resolution
+    (u0, u1), (v0, v1) = cam.u_range, cam.v_range
+    ug, vg = np.meshgrid(u0 + (np.arange(w) + 0.5) / w * (u1 - u0), v0 + (np.arange(h) + 0.5) / h * (v1 - v0))
+    plane = ug[..., None] * np.asarray(cam.axis_u) + vg[..., None] * np.asarray(cam.axis_v)
+    count = 0
+    for k in range(n):
+        p = plane + float(spec.plane_offsets[k]) * np.asarray(spec.light_dir)
+        count += int(np.all((p >= 0.0) & (p <= 1.0), axis=-1).sum())
+    got = bench.covered_texel_slices(cam, spec)
+    assert abs(got - count) <= 0.005 * count, (got, count)
