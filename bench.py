@@ -547,6 +547,7 @@ def run_ours(a, cfg, mode):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         best = None
         for _ in range(6):
+            fr.choose_march_kernel()  # throughput or latency K2 for this rank's band, by measurement
             ev[0].record(stream)
             for _ in range(3):
                 fr.build()
@@ -557,9 +558,10 @@ def run_ours(a, cfg, mode):
             worst = t.clone()
             dist.all_reduce(worst, op=dist.ReduceOp.MAX)
             if best is None or worst.item() < best[0]:
-                best = (worst.item(), list(fr.ranges))
+                best = (worst.item(), list(fr.ranges), fr.march_kernel)
             fr.rebalance(t.item())
         fr.set_ranges(best[1])
+        fr.march_kernel = best[2]
         fr.frame()
     pipelined = (world == 1 or a.build in ("replicated", "frustum")) and not a.no_pipeline
     pipe = FramePipeline(fr) if pipelined else None
@@ -678,6 +680,7 @@ def run_ours(a, cfg, mode):
             "config": workload_config(a, cfg, mode, world),
             "setup": {"build": a.build if world > 1 else "single",
                       "row_ranges": fr.ranges if fr.partition == "contiguous" else None,
+                      "march_kernel": {0: "by size", 1: "throughput", 2: "latency"}[fr.march_kernel],
                       "assemble": fr.assemble_mode if world > 1 else "none",
                       "frame_pipelining": "build(f+1) overlaps march(f)" if pipelined else "off",
                       "tile_order": "measured (previous frame)" if fr.feedback is not None else

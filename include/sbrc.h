@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 10
+#define SBRC_ABI_VERSION 11
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -207,6 +207,12 @@ typedef struct sbrc_render_params {
    * (band_rows / rank / world are then ignored). Used with a frustum-culled
    * build, whose texels only cover one contiguous screen band. */
   int32_t row_begin, row_count;
+  /* K2 kernel choice (speed only, results identical): 0 = by the rank-local
+   * image size, 1 = the throughput kernel (4 blocks/SM), 2 = the latency
+   * kernel (1 block/SM, more registers per warp; ray groups for tiny images)
+   * where one exists for the mode. A rank can measure both for its share
+   * (FrameRenderer.choose_march_kernel). */
+  int32_t march_kernel;
 } sbrc_render_params;
 
 /* ABI version of the loaded library (== SBRC_ABI_VERSION). */

@@ -16,7 +16,7 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
-ABI_VERSION = 10
+ABI_VERSION = 11
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 MAX_PEERS = 8
@@ -77,7 +77,8 @@ class SbrcRenderParams(C.Structure):
                 ("scene_light_dir", D3), ("phong", C.c_double * 4), ("voxel_size", D3),
                 ("image", C.c_void_p), ("peer_images", C.c_void_p * MAX_PEERS), ("n_peers", C.c_int32),
                 ("n_tiles", C.c_int32), ("tile_order", C.c_void_p), ("sample_count", C.c_void_p),
-                ("tile_steps", C.c_void_p), ("row_begin", C.c_int32), ("row_count", C.c_int32)]
+                ("tile_steps", C.c_void_p), ("row_begin", C.c_int32), ("row_count", C.c_int32),
+                ("march_kernel", C.c_int32)]
 
 
 class SbrcHalfAngleParams(C.Structure):

@@ -1164,6 +1164,7 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
   if (p->shading < SBRC_SHADE_NONE || p->shading > SBRC_SHADE_EXTINCTION) return SBRC_EUNSUPPORTED;
   if (p->lookup != SBRC_LOOKUP_LINEAR && p->lookup != SBRC_LOOKUP_NEAREST) return SBRC_EINVAL;
   if (!rows_ok(p)) return SBRC_EINVAL;
+  if (p->march_kernel < 0 || p->march_kernel > 2) return SBRC_EINVAL;
   if (p->shading >= SBRC_SHADE_SHADOW && p->shading <= SBRC_SHADE_CONE) {
     if (p->quads == nullptr) return SBRC_ECONFIG;
     if (!light_ok(p->light)) return SBRC_EINVAL;

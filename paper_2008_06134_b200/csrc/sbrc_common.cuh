@@ -557,7 +557,10 @@ struct MarchShape {
 };
 inline MarchShape march_shape(const sbrc_render_params& p, int local_rows) {
   MarchShape m{};
-  m.latency = march_latency_kernel(p) && (long long)p.width * local_rows <= SBRC_LATENCY_MODE_PIXELS;
+  // march_kernel: 0 = by image size (the rule below), 1 = throughput kernel, 2 = latency kernel
+  m.latency = march_latency_kernel(p) &&
+              (p.march_kernel == 2 ||
+               (p.march_kernel == 0 && (long long)p.width * local_rows <= SBRC_LATENCY_MODE_PIXELS));
   m.nw = march_wide(p.width, local_rows) ? 8 : 4;
   m.group = m.latency && (long long)p.width * local_rows <= SBRC_GROUP_PIXELS ? SBRC_LAT_GROUP : 1;
   const int tw = m.group == 1 ? SBRC_TILE_W : 4, th = (32 / m.group) / tw;

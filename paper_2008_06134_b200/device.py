@@ -325,7 +325,8 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
                   image: torch.Tensor, counter: torch.Tensor | None,
                   band_rows: int = 8, rank: int = 0, world: int = 1, voxel_size=None,
                   peer_images=(), heavy_first: bool = False,
-                  lut_host: np.ndarray | None = None, feedback=None, row_range=None) -> N.SbrcRenderParams:
+                  lut_host: np.ndarray | None = None, feedback=None, row_range=None,
+                  march_kernel: int = 0) -> N.SbrcRenderParams:
     """Pack RenderSettings + buffer into the K2 params (raycaster.py:443-469).
     ``lut_host`` (the resolved LUT on the host) enables the skip_clear hint.
     ``row_range`` = (row_begin, row_count): a contiguous share of the image
@@ -385,6 +386,7 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     p.band_rows, p.rank, p.world = int(band_rows), int(rank), int(world)
     if row_range is not None:
         p.row_begin, p.row_count = int(row_range[0]), int(row_range[1])
+    p.march_kernel = int(march_kernel)
     p.image = image.data_ptr() if image is not None else None
     if len(peer_images) > N.MAX_PEERS:
         raise ValueError(f"at most {N.MAX_PEERS} peer images")

@@ -126,6 +126,7 @@ class FrameRenderer:
         if build == "frustum" and (partition != "contiguous" or not sparse):
             raise ValueError("the frustum-culled build needs the contiguous partition and sparse K1 writes")
         self.partition = partition
+        self.march_kernel = 0  # K2 kernel choice (sbrc_render_params.march_kernel); see choose_march_kernel
         if band_rows < 8 or band_rows % 8:
             raise ValueError("band_rows must be a positive multiple of 8")
         self.group = group
@@ -226,6 +227,32 @@ class FrameRenderer:
         prof = PT.calibrated_profile(PT.row_costs_geometric(self.settings), self.ranges, times)
         self.set_ranges(PT.damped_ranges(self.ranges, PT.balanced_ranges(prof, self.world), self.height))
         return self.ranges
+
+    def choose_march_kernel(self, frames: int = 3) -> int:
+        """Time this rank's march with the throughput and the latency K2
+        kernel (CUDA events, after one warm-up each) and keep the faster —
+        which one wins depends on the share's size and on its longest rays,
+        so a contiguous band measures instead of trusting the size rule.
+        Local (no collective); results are identical either way."""
+        stream = torch.cuda.current_stream(self.dev)
+        times = {}
+        for k in (1, 2):
+            self.march_kernel = k
+            self._params.clear()
+            self.build()
+            self.march(False)  # warm-up (and a fresh heavy-first table for this grid)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(frames):
+                self.march(False)
+            e1.record(stream)
+            e1.synchronize()
+            times[k] = e0.elapsed_time(e1) / frames
+        self.march_kernel = min(times, key=times.get)
+        self._params.clear()
+        if self.feedback is not None:
+            self.feedback.grid = None
+        return self.march_kernel
 
     # -------------------------------------------------------------- p2p
     def _setup_p2p(self) -> None:
@@ -384,7 +411,8 @@ class FrameRenderer:
                 peer_images=self._peers[key[1]] if p2p else (),
                 heavy_first=(self.feedback is not None or self.world != 2) if self.heavy_first is None
                 else self.heavy_first,
-                lut_host=self.lut_host, feedback=self.feedback, row_range=self.row_range)
+                lut_host=self.lut_host, feedback=self.feedback, row_range=self.row_range,
+                march_kernel=self.march_kernel)
             self._params[key] = params
         elif self.feedback is not None and self.feedback.steps is not None:
             self.feedback.steps.zero_()

@@ -60,22 +60,27 @@ def main():
         shape = PT.row_costs_geometric(settings)
         ranges = PT.balanced_ranges(shape, world)
         history = []
+        kernels = [0] * world
         for _ in range(6 if world > 1 else 0):  # re-cut by measured per-rank frame times
             times = []
             for r in range(world):
                 fr = rank_renderer(dvol, scene, world, r, ranges)
+                if world > 1:
+                    kernels[r] = fr.choose_march_kernel()
                 times.append(timed(lambda: (fr.build(), fr.march(False)), k=5))
                 del fr
                 gc.collect()
-            history.append({"ranges": ranges, "max_ms": max(times), "times": times})
+            history.append({"ranges": ranges, "max_ms": max(times), "times": times, "kernels": list(kernels)})
             ranges = PT.damped_ranges(ranges, PT.balanced_ranges(PT.calibrated_profile(shape, ranges, times), world),
                                       settings.viewport[1])
-        if history:  # the best cut seen
-            ranges = min(history, key=lambda e: e["max_ms"])["ranges"]
+        if history:  # the best cut seen, with the kernels each rank chose for it
+            best = min(history, key=lambda e: e["max_ms"])
+            ranges, kernels = best["ranges"], best["kernels"]
         ranks = []
         same = True
         for r in range(world):
             fr = rank_renderer(dvol, scene, world, r, ranges)
+            fr.march_kernel = kernels[r]
             b, n = fr.row_range
             fr.build()
             fr.march(False)
@@ -88,7 +93,7 @@ def main():
             pipe.drain()
             torch.cuda.synchronize()
             same &= bool(torch.equal(fr.chunk[:n], ref[b:b + n]))
-            ranks.append({"rows": [b, n], "build_ms": t_build, "march_ms": t_march, "serial_ms": t_serial,
+            ranks.append({"rows": [b, n], "march_kernel": kernels[r], "build_ms": t_build, "march_ms": t_march, "serial_ms": t_serial,
                           "pipelined_ms": t_pipe})
             del pipe, fr
             gc.collect()

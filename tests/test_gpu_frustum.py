@@ -174,3 +174,23 @@ def test_frustum_config3_full_size(torch):
         b, n = fr.row_range
         assert torch.equal(fr.chunk[:n], ref[b:b + n]), (r, ranges)
         del fr
+
+
+@pytest.mark.parametrize("mode", ["cone", "shell", "sbrc_shadow"])
+def test_forced_march_kernel_identical(torch, mode):
+    """sbrc_render_params.march_kernel (throughput / latency K2, and the
+    measured choice of FrameRenderer.choose_march_kernel) never changes the
+    image."""
+    import paper_2008_06134_b200 as sb
+    from paper_2008_06134_b200.frame import FrameRenderer
+    g = load_golden("config1")
+    v, tf, cam, spec, settings_for = scene_from_golden(g)
+    s = settings_for(mode)
+    ref = sb.render_device(v, tf, s, sb.build_attenuation_buffer(v, tf, cam, spec))
+    fr = FrameRenderer(v, tf, cam, spec, s)
+    for k in (1, 2, 0):
+        fr.march_kernel = k
+        fr._params.clear()
+        assert torch.equal(fr.frame(), ref), k
+    assert fr.choose_march_kernel() in (1, 2)
+    assert torch.equal(fr.frame(), ref)
