@@ -511,10 +511,19 @@ def run_ours(a, cfg, mode):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SBRC_BENCH_SAME_GPU=1 + SBRC_BENCH_BACKEND=gloo: every rank on cuda:0 — a
+    # control-flow check of the multi-rank bench on a one-GPU box (NCCL needs
+    # distinct GPUs); timings of such a run mean nothing.
+    if os.environ.get("SBRC_BENCH_SAME_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SBRC_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2008_06134_b200 as sb
     from paper_2008_06134_b200.frame import FramePipeline, FrameRenderer
