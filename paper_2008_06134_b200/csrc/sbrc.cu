@@ -18,15 +18,17 @@ namespace {
 // the cube, alpha = lut(trilinear(p)) and T *= 1 - alpha. Texels are
 // independent, so no grid-wide barrier or per-slice launch is needed. The
 // quad of layer k needs layer k+1, so it is emitted one slice late.
-// K1 block: 4 warps (light rows), compiled for 6 blocks/SM (80 registers,
-// 24 warps/SM, as with 8-warp blocks) — the finer blocks even out the last
-// wave of uneven texel rows (A/B in profiles/r01_notes.md: config 3 build
-// 0.466 -> 0.417 ms, config 2 0.209 -> 0.179, config 4 3.61 -> 3.47).
+// K1 block: 4 warps (light rows) — the finer blocks even out the last wave
+// of uneven texel rows (A/B in profiles/r01_notes.md: config 3 build 0.466
+// -> 0.417 ms, config 2 0.209 -> 0.179, config 4 3.61 -> 3.47) — compiled
+// for 8 blocks/SM (64 registers, 32 warps/SM, one slice's gathers at a time;
+// vs 6 blocks/SM with two slices in flight: config 3 0.309 -> 0.299 ms,
+// config 2 0.136 -> 0.132, config 4 2.15 -> 2.12, profiles/r2_notes.md).
 #ifndef SBRC_BUILD_ROWS
 #define SBRC_BUILD_ROWS 4
 #endif
 #ifndef SBRC_BUILD_MINB
-#define SBRC_BUILD_MINB 6
+#define SBRC_BUILD_MINB 8
 #endif
 // Async gather pipeline (float32 volumes): the 8 corner voxels of slice
 // k + D - 1 are copied global -> shared with cp.async (LDGSTS, no register

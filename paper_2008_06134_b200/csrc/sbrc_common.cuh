@@ -66,7 +66,7 @@
 #define SBRC_CONE_RING_SERIAL 0  // 1: one cone ring's loads in flight at a time (fewer registers)
 #endif
 #ifndef SBRC_BUILD_UNROLL
-#define SBRC_BUILD_UNROLL 2  // slices whose gathers are in flight together in K1
+#define SBRC_BUILD_UNROLL 1  // slices whose gathers are issued together in K1 (1 + 8 blocks/SM: -3%, r3h)
 #endif
 
 // Checked build (SBRC_CHECKED=1, scripts/checked_run.py): every global
