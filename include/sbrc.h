@@ -245,6 +245,14 @@ int sbrc_normalize_f32(float* data, int64_t n, float lo, float range, void* stre
  * float32 division by 255 / 65535, bit-identical to numpy). */
 int sbrc_widen_volume(const void* src, int voxel_type, int64_t n, float* dst, void* stream);
 
+/* Volume layout the kernels of this library read: 0 = linear (nz, ny, nx),
+ * 1 = 8^3-cell bricks with a one-voxel apron (an A/B build, SBRC_BRICK=1);
+ * sbrc_volume.data must then point at sbrc_brick_pack's output, of
+ * sbrc_brick_elems(nx, ny, nz) voxels. */
+int sbrc_volume_layout(void);
+int64_t sbrc_brick_elems(int nx, int ny, int nz);
+int sbrc_brick_pack(const void* src, int voxel_type, int nx, int ny, int nz, void* dst, void* stream);
+
 /* Heavy-first dispatch table from measured tile costs (schedule.TileFeedback):
  * order[0..n) = tile indices by decreasing steps[i], ties by increasing index
  * (deterministic). Device pointers; replaces a stable descending argsort. */

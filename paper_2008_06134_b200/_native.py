@@ -33,7 +33,7 @@ EXPORTS = ("sbrc_abi_version", "sbrc_strerror", "sbrc_struct_size", "sbrc_volume
            "sbrc_normalize_f32", "sbrc_half_angle", "sbrc_ipc_alloc", "sbrc_ipc_free", "sbrc_ipc_handle",
            "sbrc_ipc_open", "sbrc_ipc_close", "sbrc_march_grid", "sbrc_local_rows",
            "sbrc_render_grid", "sbrc_host_device_pointer", "sbrc_debug_violations", "sbrc_widen_volume",
-           "sbrc_tile_order", "sbrc_permute_rows")
+           "sbrc_tile_order", "sbrc_permute_rows", "sbrc_volume_layout", "sbrc_brick_elems", "sbrc_brick_pack")
 
 D3 = C.c_double * 3
 D2 = C.c_double * 2
@@ -123,6 +123,10 @@ def _load() -> C.CDLL:
     lib.sbrc_normalize_f32.argtypes = [C.c_void_p, C.c_int64, C.c_float, C.c_float, C.c_void_p]
     lib.sbrc_widen_volume.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
     lib.sbrc_tile_order.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    lib.sbrc_volume_layout.restype = C.c_int
+    lib.sbrc_brick_elems.argtypes = [C.c_int, C.c_int, C.c_int]
+    lib.sbrc_brick_elems.restype = C.c_int64
+    lib.sbrc_brick_pack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     lib.sbrc_permute_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
     lib.sbrc_shadow_oracle.argtypes = [C.POINTER(SbrcVolume), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_double, C.c_void_p, C.c_void_p]

@@ -664,6 +664,22 @@ __global__ void __launch_bounds__(256) widen_kernel(const T* __restrict__ src, f
     dst[i] = __fdiv_rn((float)src[i], scale);
 }
 
+// Brick repack (SBRC_BRICK builds): dst element (brick, lz, ly, lx) = src
+// voxel (min(8 bx + lx, nx-1), ...) — the apron replicates the far faces.
+template <typename T>
+__global__ void __launch_bounds__(256) brick_pack_kernel(const T* __restrict__ src, T* __restrict__ dst, int nx,
+                                                        int ny, int nz, long long total) {
+  const int nbx = brick_count(nx), nby = brick_count(ny);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long brick = i / kBrickN;
+    const int e = (int)(i - brick * kBrickN);
+    const int lx = e % kBrickS, ly = (e / kBrickS) % kBrickS, lz = e / (kBrickS * kBrickS);
+    const int bx = (int)(brick % nbx), by = (int)((brick / nbx) % nby), bz = (int)(brick / ((long long)nbx * nby));
+    const int x = min(bx * kBrick + lx, nx - 1), y = min(by * kBrick + ly, ny - 1), z = min(bz * kBrick + lz, nz - 1);
+    dst[i] = src[((size_t)z * ny + y) * nx + x];
+  }
+}
+
 // Heavy-first order from measured tile costs (schedule.TileFeedback): tiles
 // by decreasing steps, ties by increasing index — every key
 // (~steps << 32 | index) is unique, so its rank among all keys is its slot
@@ -880,7 +896,7 @@ void launch_build(const sbrc_build_params& p, cudaStream_t s) {
   if constexpr (VT == SBRC_VOXEL_F32) {
     int4 box;
     size_t smem;
-    PFN_cuTensorMapEncodeTiled enc = SBRC_BUILD_TMA ? tensor_map_encoder() : nullptr;
+    PFN_cuTensorMapEncodeTiled enc = SBRC_BUILD_TMA && !SBRC_BRICK ? tensor_map_encoder() : nullptr;
     if (enc != nullptr && unit_box(p.volume) && tma_plan(p, &box, &smem)) {
       const cuuint64_t gdim[3] = {(cuuint64_t)p.volume.nx, (cuuint64_t)p.volume.ny, (cuuint64_t)p.volume.nz};
       const cuuint64_t gstride[2] = {(cuuint64_t)p.volume.nx * 4, (cuuint64_t)p.volume.nx * p.volume.ny * 4};
@@ -896,7 +912,7 @@ void launch_build(const sbrc_build_params& p, cudaStream_t s) {
       }
     }
   }
-  constexpr int D = VT == SBRC_VOXEL_F32 ? SBRC_BUILD_ASYNC : 0;
+  constexpr int D = VT == SBRC_VOXEL_F32 && !SBRC_BRICK ? SBRC_BUILD_ASYNC : 0;
   if (unit_box(p.volume)) build_kernel<VT, true, D><<<grid, block, 0, s>>>(p, tmap, none);
   else build_kernel<VT, false, D><<<grid, block, 0, s>>>(p, tmap, none);
 }
@@ -1065,6 +1081,36 @@ int sbrc_widen_volume(const void* src, int voxel_type, int64_t n, float* dst, vo
     widen_kernel<unsigned char><<<148 * 8, 256, 0, s>>>(static_cast<const unsigned char*>(src), dst, n, 255.0f);
   else
     widen_kernel<unsigned short><<<148 * 8, 256, 0, s>>>(static_cast<const unsigned short*>(src), dst, n, 65535.0f);
+  return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
+}
+
+int sbrc_volume_layout(void) { return SBRC_BRICK; }
+
+int64_t sbrc_brick_elems(int nx, int ny, int nz) {
+  if (nx < 2 || ny < 2 || nz < 2) return -1;
+  return (int64_t)brick_count(nx) * brick_count(ny) * brick_count(nz) * kBrickN;
+}
+
+int sbrc_brick_pack(const void* src, int voxel_type, int nx, int ny, int nz, void* dst, void* stream) {
+  const int64_t total = sbrc_brick_elems(nx, ny, nz);
+  if (src == nullptr || dst == nullptr || total < 0) return SBRC_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = 148 * 8;
+  switch (voxel_type) {
+    case SBRC_VOXEL_F32:
+      brick_pack_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(src), static_cast<float*>(dst), nx, ny,
+                                                     nz, total);
+      break;
+    case SBRC_VOXEL_U8:
+      brick_pack_kernel<unsigned char><<<grid, 256, 0, s>>>(static_cast<const unsigned char*>(src),
+                                                             static_cast<unsigned char*>(dst), nx, ny, nz, total);
+      break;
+    case SBRC_VOXEL_U16:
+      brick_pack_kernel<unsigned short><<<grid, 256, 0, s>>>(static_cast<const unsigned short*>(src),
+                                                              static_cast<unsigned short*>(dst), nx, ny, nz, total);
+      break;
+    default: return SBRC_EINVAL;
+  }
   return cudaGetLastError() == cudaSuccess ? SBRC_OK : SBRC_ECUDA;
 }
 

@@ -157,6 +157,25 @@ template <> struct Voxel<SBRC_VOXEL_U16> {
 // nx*ny*nz < 2^32). UNIT: the volume box is the unit cube (box_lo = 0,
 // box_hi = 1: every cubic dataset), where local = (p - 0)/1 = p exactly and
 // the clip is a no-op inside the cube.
+// Brick layout (SBRC_BRICK = 1, an A/B build): the volume is stored as
+// bricks of 8^3 cells, each holding its 9^3 corner voxels (a one-voxel
+// apron on the +x/+y/+z sides, edge-replicated at the volume's far faces),
+// bricks and voxels x-fastest. A cell's 8 corners then sit in one 2.8 KB
+// brick (rows y, y+1 are 36 B apart, slices z, z+1 324 B) instead of four
+// rows up to nx*ny*4 bytes apart. 729/512 = 1.42x the voxel bytes.
+#ifndef SBRC_BRICK
+#define SBRC_BRICK 0
+#endif
+constexpr int kBrick = 8, kBrickS = 9, kBrickN = 729;
+__host__ __device__ __forceinline__ int brick_count(int n) { return n > 1 ? (n - 2) / kBrick + 1 : 1; }
+// element offset of voxel (x, y, z) in brick (bx, by, bz): local coordinates in 0..8
+__device__ __forceinline__ unsigned brick_voxel(const sbrc_volume& v, int x, int y, int z) {
+  const int bx = min(x / kBrick, brick_count(v.nx) - 1), by = min(y / kBrick, brick_count(v.ny) - 1),
+            bz = min(z / kBrick, brick_count(v.nz) - 1);
+  const unsigned brick = ((unsigned)bz * brick_count(v.ny) + by) * brick_count(v.nx) + bx;
+  return brick * kBrickN + ((unsigned)(z - bz * kBrick) * kBrickS + (y - by * kBrick)) * kBrickS + (x - bx * kBrick);
+}
+
 template <int VT>
 struct Cell {
   typename Voxel<VT>::T r[8];  // d000 d100 d010 d110 d001 d101 d011 d111
@@ -180,6 +199,31 @@ __device__ __forceinline__ void cell_fetch(const sbrc_volume& v, double px, doub
   }
   const T* base = reinterpret_cast<const T*>(v.data);
   const unsigned nx = (unsigned)v.nx, nxy = (unsigned)v.nx * (unsigned)v.ny;
+  if (SBRC_BRICK) {
+    if ((unsigned)lo[0] < (unsigned)(v.nx - 1) && (unsigned)lo[1] < (unsigned)(v.ny - 1) &&
+        (unsigned)lo[2] < (unsigned)(v.nz - 1)) {
+      // interior: the cell's brick holds all 8 corners (apron)
+      const unsigned bx = (unsigned)lo[0] / kBrick, by = (unsigned)lo[1] / kBrick, bz = (unsigned)lo[2] / kBrick;
+      const unsigned brick = (bz * (unsigned)brick_count(v.ny) + by) * (unsigned)brick_count(v.nx) + bx;
+      const T* c = base + (brick * kBrickN + (((unsigned)lo[2] - bz * kBrick) * kBrickS + ((unsigned)lo[1] - by * kBrick)) *
+                                                 kBrickS + ((unsigned)lo[0] - bx * kBrick));
+      cl.r[0] = __ldg(c); cl.r[1] = __ldg(c + 1); cl.r[2] = __ldg(c + kBrickS); cl.r[3] = __ldg(c + kBrickS + 1);
+      const T* cz = c + kBrickS * kBrickS;
+      cl.r[4] = __ldg(cz); cl.r[5] = __ldg(cz + 1); cl.r[6] = __ldg(cz + kBrickS); cl.r[7] = __ldg(cz + kBrickS + 1);
+    } else {
+      int a[3], b[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a[c] = min(max(lo[c], 0), dims[c] - 1);
+        b[c] = min(max(lo[c] + 1, 0), dims[c] - 1);
+      }
+      cl.r[0] = __ldg(base + brick_voxel(v, a[0], a[1], a[2])); cl.r[1] = __ldg(base + brick_voxel(v, b[0], a[1], a[2]));
+      cl.r[2] = __ldg(base + brick_voxel(v, a[0], b[1], a[2])); cl.r[3] = __ldg(base + brick_voxel(v, b[0], b[1], a[2]));
+      cl.r[4] = __ldg(base + brick_voxel(v, a[0], a[1], b[2])); cl.r[5] = __ldg(base + brick_voxel(v, b[0], a[1], b[2]));
+      cl.r[6] = __ldg(base + brick_voxel(v, a[0], b[1], b[2])); cl.r[7] = __ldg(base + brick_voxel(v, b[0], b[1], b[2]));
+    }
+    return;
+  }
   if ((unsigned)lo[0] < (unsigned)(v.nx - 1) && (unsigned)lo[1] < (unsigned)(v.ny - 1) &&
       (unsigned)lo[2] < (unsigned)(v.nz - 1)) {
     // interior: the 2x2x2 cell without clamping

@@ -86,9 +86,24 @@ class DeviceVolume:
     def nbytes(self) -> int:
         return self.data.numel() * self.data.element_size()
 
+    @property
+    def kernel_data(self) -> torch.Tensor:
+        """The voxels in the layout the loaded library's kernels read: ``data``
+        itself (linear), or — in a brick-layout A/B build (sbrc_volume_layout()
+        == 1) — a bricked copy made once on the device."""
+        if N.lib.sbrc_volume_layout() == 0:
+            return self.data
+        if getattr(self, "_bricked", None) is None:
+            nx, ny, nz = self.dims
+            out = torch.empty(int(N.lib.sbrc_brick_elems(nx, ny, nz)), dtype=self.data.dtype, device=self.data.device)
+            N.check(N.lib.sbrc_brick_pack(self.data.data_ptr(), self.voxel_type, nx, ny, nz, out.data_ptr(),
+                                          current_stream_handle()), "sbrc_brick_pack")
+            self._bricked = out
+        return self._bricked
+
     def struct(self) -> N.SbrcVolume:
         s = N.SbrcVolume()
-        s.data = self.data.data_ptr()
+        s.data = self.kernel_data.data_ptr()
         s.nx, s.ny, s.nz = self.dims
         s.voxel_type = self.voxel_type
         s.box_lo[:] = [float(x) for x in self.box_lo]
@@ -396,7 +411,7 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     p.sample_count = counter.data_ptr() if counter is not None else None
     # The struct holds raw device addresses: it keeps the tensors behind them
     # alive for as long as a caller caches it (FrameRenderer, FramePipeline).
-    keep = [dvol.data, lut_dev, quads_dev, image, counter]
+    keep = [dvol.data, dvol.kernel_data, lut_dev, quads_dev, image, counter]
     if heavy_first:  # dispatch table over the exact grid sbrc_render will launch
         grid = N.render_grid(p)
         order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, grid, row_range)
