@@ -138,6 +138,9 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS,
   auto put = [&](int kk, const float4& q) {  // texel quad, or its layer-k value in the plain layout
     SBRC_CHECK(kk >= 0 && kk < L.n_slices && x < L.width && y < P.row_end, 2);
     if (plain) prow[(size_t)kk * ks + x] = q.x;
+    else if (SBRC_PAIRS)  // layer-pair A/B build: (I[k], I[k+1]) of this texel, dense at the quad offsets
+      reinterpret_cast<float2*>(P.quads)[(size_t)(y - P.row_begin) * (size_t)P.quad_row_stride + (size_t)kk * ks + x] =
+          make_float2(q.x, q.y);
     else row[(size_t)kk * ks + x] = q;
   };
   const float* tab = reinterpret_cast<const float*>(u8tab);

@@ -443,6 +443,26 @@ __device__ __forceinline__ QuadTex make_quad_tex(const sbrc_render_params& P) {
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b, fmaf(-t, a, a)); }
 
+// Layer-pair layout (SBRC_PAIRS = 1, an A/B build): the stack is stored as
+// float2 (I[k][y][x], I[k+1][y][x]) per texel, densely at the same (k, y, x)
+// offsets the quads use (2x instead of 4x the plain stack); a two-row tap
+// then takes four 8-byte loads instead of two 16-byte quads. Valid for W >= 2.
+#ifndef SBRC_PAIRS
+#define SBRC_PAIRS 0
+#endif
+// rows y and y+1 of the tap at quad offset `off` as (I[k][x], I[k+1][x], I[k][x+1], I[k+1][x+1])
+__device__ __forceinline__ void tap_rows(const float4* q, size_t off, size_t row_step, float4& r0, float4& r1) {
+  if (SBRC_PAIRS) {
+    const float2* p = reinterpret_cast<const float2*>(q) + off;
+    const float2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + row_step), d = __ldg(p + row_step + 1);
+    r0 = make_float4(a.x, a.y, b.x, b.y);
+    r1 = make_float4(c.x, c.y, d.x, d.y);
+  } else {
+    r0 = __ldg(q + off);
+    r1 = __ldg(q + off + row_step);
+  }
+}
+
 #ifndef SBRC_PREC
 #define SBRC_PREC 0  // experiment: 0 exact float64 sample path; 1 float32 colour; 2 float32 sample
 #endif
@@ -485,10 +505,10 @@ __device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float 
     ka = fminf(floor_f(li).f, t.ka_max);
     f = li - ka;
   }
-  const float4* p = t.q + ((unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa);
-  SBRC_CHECK((unsigned long long)(p - t.q) + t.qy1_64 <= t.last && ka >= 0.f && ya >= 0.f && xa >= 0.f, 1);
-  const float4 r0 = __ldg(p);
-  const float4 r1 = __ldg(p + t.qy1_64);
+  const unsigned off = (unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa;
+  SBRC_CHECK((unsigned long long)off + t.qy1_64 <= t.last && ka >= 0.f && ya >= 0.f && xa >= 0.f, 1);
+  float4 r0, r1;
+  tap_rows(t.q, off, t.qy1_64, r0, r1);
   const float a0 = lerpf(r0.x, r0.z, fx), a1 = lerpf(r1.x, r1.z, fx);  // layer ka, rows y, y+1
   const float v0 = lerpf(a0, a1, fy);
   if (LOOKUP == SBRC_LOOKUP_NEAREST) return v0;
@@ -504,10 +524,10 @@ __device__ __forceinline__ void interior_tap(const QuadTex& t, unsigned kbase, f
                                              float& v1) {
   const FloorF xl = floor_f(tx), yl = floor_f(ty);
   const float fx = tx - xl.f, fy = ty - yl.f;
-  const float4* p = t.q + (kbase + (unsigned)yl.i * t.qy + (unsigned)xl.i);
-  SBRC_CHECK(p >= t.q && (unsigned long long)(p - t.q) + t.qy64 <= t.last, 1);
-  const float4 r0 = __ldg(p);
-  const float4 r1 = __ldg(p + t.qy64);
+  const unsigned off = kbase + (unsigned)yl.i * t.qy + (unsigned)xl.i;
+  SBRC_CHECK((unsigned long long)off + t.qy64 <= t.last, 1);
+  float4 r0, r1;
+  tap_rows(t.q, off, t.qy64, r0, r1);
   v0 += lerpf(lerpf(r0.x, r0.z, fx), lerpf(r1.x, r1.z, fx), fy);
   v1 += lerpf(lerpf(r0.y, r0.w, fx), lerpf(r1.y, r1.w, fx), fy);
 }
@@ -546,10 +566,10 @@ __device__ __forceinline__ float2 interior_tap2(const QuadTex& t, unsigned kbase
     xi = (unsigned)xl.i;
     yi = (unsigned)yl.i;
   }
-  const float4* q = t.q + (kbase + yi * t.qy + xi);
-  SBRC_CHECK(q >= t.q && (unsigned long long)(q - t.q) + t.qy64 <= t.last, 1);
-  const float4 r0 = __ldg(q);
-  const float4 r1 = __ldg(q + t.qy64);
+  const unsigned off = kbase + yi * t.qy + xi;
+  SBRC_CHECK((unsigned long long)off + t.qy64 <= t.last, 1);
+  float4 r0, r1;
+  tap_rows(t.q, off, t.qy64, r0, r1);
   if (SBRC_PACKED & 2) {
     const float2 a = lerp2(make_float2(r0.x, r0.y), make_float2(r0.z, r0.w), f.x);
     const float2 b = lerp2(make_float2(r1.x, r1.y), make_float2(r1.z, r1.w), f.x);
