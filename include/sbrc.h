@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SBRC_ABI_VERSION 11
+#define SBRC_ABI_VERSION 12
 #define SBRC_MAX_SHELLS 8   /* ShellKernel radii (raycaster.py:92-109) */
 #define SBRC_MAX_ANGLES 16  /* ConeKernel angles (raycaster.py:113-124) */
 #define SBRC_LUT_SIZE 256   /* transfer.py:16 */
@@ -140,6 +140,10 @@ typedef struct sbrc_build_params {
    * written are identical to a full build. */
   int32_t n_clip;
   double clip[SBRC_MAX_CLIP][4];
+  /* Stack layout: 0 = texel quads (above); 1 = layer pairs: float2
+   * (I[k][y][x], I[k+1][y][x]) per texel at the same (k, y, x) offsets, in
+   * float2 units (half the bytes; read by an sbrc_shadow march only). */
+  int32_t quad_layout;
 } sbrc_build_params;
 
 typedef struct sbrc_render_params {
@@ -213,6 +217,10 @@ typedef struct sbrc_render_params {
    * where one exists for the mode. A rank can measure both for its share
    * (FrameRenderer.choose_march_kernel). */
   int32_t march_kernel;
+  /* Layout of `quads` (sbrc_build_params.quad_layout): 1 = layer pairs, for
+   * shading == SBRC_SHADE_SHADOW and width >= 2 only (the single-lookup
+   * march reads half the bytes; results identical). */
+  int32_t quad_layout;
 } sbrc_render_params;
 
 /* ABI version of the loaded library (== SBRC_ABI_VERSION). */

@@ -16,7 +16,7 @@ from .scene import ConfigError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SBRC_LIB") or os.path.join(_HERE, "_sbrc.so")  # SBRC_LIB: A/B experiments
 
-ABI_VERSION = 11
+ABI_VERSION = 12
 MAX_SHELLS = 8
 MAX_ANGLES = 16
 MAX_PEERS = 8
@@ -57,7 +57,7 @@ class SbrcBuildParams(C.Structure):
                 ("quads", C.c_void_p), ("quad_layer_stride", C.c_int64), ("quad_row_stride", C.c_int64),
                 ("write_reach", C.c_double), ("write_below", C.c_int32), ("write_above", C.c_int32),
                 ("write_sparse", C.c_int32), ("output_plain", C.c_int32),
-                ("n_clip", C.c_int32), ("clip", (C.c_double * 4) * MAX_CLIP)]
+                ("n_clip", C.c_int32), ("clip", (C.c_double * 4) * MAX_CLIP), ("quad_layout", C.c_int32)]
 
 
 class SbrcRenderParams(C.Structure):
@@ -78,7 +78,7 @@ class SbrcRenderParams(C.Structure):
                 ("image", C.c_void_p), ("peer_images", C.c_void_p * MAX_PEERS), ("n_peers", C.c_int32),
                 ("n_tiles", C.c_int32), ("tile_order", C.c_void_p), ("sample_count", C.c_void_p),
                 ("tile_steps", C.c_void_p), ("row_begin", C.c_int32), ("row_count", C.c_int32),
-                ("march_kernel", C.c_int32)]
+                ("march_kernel", C.c_int32), ("quad_layout", C.c_int32)]
 
 
 class SbrcHalfAngleParams(C.Structure):

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS,
   auto put = [&](int kk, const float4& q) {  // texel quad, or its layer-k value in the plain layout
     SBRC_CHECK(kk >= 0 && kk < L.n_slices && x < L.width && y < P.row_end, 2);
     if (plain) prow[(size_t)kk * ks + x] = q.x;
-    else if (SBRC_PAIRS)  // layer-pair A/B build: (I[k], I[k+1]) of this texel, dense at the quad offsets
+    else if (SBRC_PAIRS || P.quad_layout == 1)  // layer pairs: (I[k], I[k+1]) of this texel at the quad offset
       reinterpret_cast<float2*>(P.quads)[(size_t)(y - P.row_begin) * (size_t)P.quad_row_stride + (size_t)kk * ks + x] =
           make_float2(q.x, q.y);
     else row[(size_t)kk * ks + x] = q;
@@ -1043,6 +1043,7 @@ int sbrc_build(const sbrc_build_params* p, void* stream) {
   if (p->light.plane_offsets == nullptr || p->alpha_lut == nullptr || p->quads == nullptr) return SBRC_EINVAL;
   if (p->row_begin < 0 || p->row_end > p->light.height || p->row_begin >= p->row_end) return SBRC_EINVAL;
   if (p->n_clip < 0 || p->n_clip > SBRC_MAX_CLIP || (p->n_clip > 0 && !p->write_sparse)) return SBRC_EINVAL;
+  if (p->quad_layout < 0 || p->quad_layout > 1 || (p->quad_layout == 1 && p->output_plain)) return SBRC_EINVAL;
   if (p->quad_layer_stride < 1 || p->quad_row_stride < p->light.width) return SBRC_EINVAL;
   if (p->compensation_n < 0.0) return SBRC_EINVAL;
   if (p->write_sparse && (!(p->write_reach >= 0.0) || p->write_below < 0 || p->write_above < 0)) return SBRC_EINVAL;
@@ -1140,6 +1141,7 @@ int sbrc_light_factor(const sbrc_render_params* p, const double* pts, int64_t m,
   if (p->lookup != SBRC_LOOKUP_LINEAR && p->lookup != SBRC_LOOKUP_NEAREST) return SBRC_EINVAL;
   if (p->quads == nullptr) return SBRC_ECONFIG;
   if (!light_ok(p->light) || !quads_ok(p->light, p->quad_layer_stride, p->quad_row_stride)) return SBRC_EINVAL;
+  if (p->quad_layout != 0) return SBRC_EINVAL;  // the point API reads texel quads
   if (p->shading == SBRC_SHADE_SHELL && (p->shell_count < 1 || p->shell_count > SBRC_MAX_SHELLS)) return SBRC_EINVAL;
   if (p->shading == SBRC_SHADE_CONE && (p->cone_axis_samples < 1 || p->cone_angle_count < 1 ||
                                         p->cone_angle_count > SBRC_MAX_ANGLES))
@@ -1216,6 +1218,9 @@ int sbrc_render(const sbrc_render_params* p, void* stream) {
   if (p->lookup != SBRC_LOOKUP_LINEAR && p->lookup != SBRC_LOOKUP_NEAREST) return SBRC_EINVAL;
   if (!rows_ok(p)) return SBRC_EINVAL;
   if (p->march_kernel < 0 || p->march_kernel > 2) return SBRC_EINVAL;
+  if (p->quad_layout < 0 || p->quad_layout > 1 ||
+      (p->quad_layout == 1 && (p->shading != SBRC_SHADE_SHADOW || p->light.width < 2)))
+    return SBRC_EINVAL;
   if (p->shading >= SBRC_SHADE_SHADOW && p->shading <= SBRC_SHADE_CONE) {
     if (p->quads == nullptr) return SBRC_ECONFIG;
     if (!light_ok(p->light)) return SBRC_EINVAL;

@@ -407,6 +407,7 @@ __device__ double phong_scalar(const sbrc_render_params& P, const float* u8tab, 
 // and the layer coordinate li = idx - 0.5 (lightbuffer.py:241-242, :279).
 struct QuadTex {
   const float4* q;
+  bool pairs;            // sbrc_render_params.quad_layout == 1: float2 layer pairs (sbrc_shadow only)
   unsigned qk, qy;       // layer / row strides in quads
   size_t qy64, qy1_64;   // row step as a 64-bit value; qy1_64: step to row y+1 (0 if H == 1)
   float txmax, tymax;    // footprint: u in [0,1]  <=>  tx in [-0.5, W-0.5]
@@ -425,6 +426,7 @@ __device__ __forceinline__ QuadTex make_quad_tex(const sbrc_render_params& P) {
   const sbrc_light_frame& LF = P.light;
   QuadTex t;
   t.q = reinterpret_cast<const float4*>(P.quads);
+  t.pairs = P.quad_layout == 1;
   t.qk = (unsigned)P.quad_layer_stride;
   t.qy = (unsigned)P.quad_row_stride;
   t.qy64 = (size_t)P.quad_row_stride;
@@ -451,8 +453,9 @@ __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(
 #define SBRC_PAIRS 0
 #endif
 // rows y and y+1 of the tap at quad offset `off` as (I[k][x], I[k+1][x], I[k][x+1], I[k+1][x+1])
-__device__ __forceinline__ void tap_rows(const float4* q, size_t off, size_t row_step, float4& r0, float4& r1) {
-  if (SBRC_PAIRS) {
+__device__ __forceinline__ void tap_rows(const float4* q, size_t off, size_t row_step, float4& r0, float4& r1,
+                                         bool pairs = false) {
+  if (SBRC_PAIRS || pairs) {
     const float2* p = reinterpret_cast<const float2*>(q) + off;
     const float2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + row_step), d = __ldg(p + row_step + 1);
     r0 = make_float4(a.x, a.y, b.x, b.y);
@@ -488,7 +491,9 @@ __device__ __forceinline__ float cell_combine_f(const Cell<VT>& cl, const float*
 // (:274-276). Index clamping (clip(x0,0,W-1), clip(x0+1,0,W-1)) is replaced
 // by clamping the cell to [0, W-2] and saturating the weight, which selects
 // the same texel values.
-template <int LOOKUP>
+// PAIRS_OK: the caller accepts a layer-pair buffer (t.pairs, a uniform
+// runtime choice; instantiated only for the one-lookup sbrc_shadow march).
+template <int LOOKUP, bool PAIRS_OK = false>
 __device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float ty, float li_raw) {
   // li_raw: idx - 0.5 for linear lookups, idx for nearest
   if (!(tx >= -0.5f && tx <= t.txmax && ty >= -0.5f && ty <= t.tymax)) return 1.0f;
@@ -508,7 +513,7 @@ __device__ __forceinline__ float light_lookup(const QuadTex& t, float tx, float 
   const unsigned off = (unsigned)ka * t.qk + (unsigned)ya * t.qy + (unsigned)xa;
   SBRC_CHECK((unsigned long long)off + t.qy1_64 <= t.last && ka >= 0.f && ya >= 0.f && xa >= 0.f, 1);
   float4 r0, r1;
-  tap_rows(t.q, off, t.qy1_64, r0, r1);
+  tap_rows(t.q, off, t.qy1_64, r0, r1, PAIRS_OK && t.pairs);
   const float a0 = lerpf(r0.x, r0.z, fx), a1 = lerpf(r1.x, r1.z, fx);  // layer ka, rows y, y+1
   const float v0 = lerpf(a0, a1, fy);
   if (LOOKUP == SBRC_LOOKUP_NEAREST) return v0;
@@ -889,7 +894,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
           const float li = fmaf(jf, flis, fli0);
           float scalar;
           if (SHADING == SBRC_SHADE_SHADOW) {
-            scalar = light_lookup<LOOKUP>(tex, tx, ty, li);
+            scalar = light_lookup<LOOKUP, true>(tex, tx, ty, li);
           } else if (SHADING == SBRC_SHADE_SHELL) {
             float acc = 0.0f;
             const int nsh = NSHELL > 0 ? NSHELL : P.shell_count;

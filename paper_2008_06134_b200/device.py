@@ -262,11 +262,19 @@ def light_frame(cam, spec, offsets_dev: torch.Tensor | None) -> N.SbrcLightFrame
 
 
 def quad_strides(quads: torch.Tensor) -> tuple[int, int]:
-    """(layer, row) strides in float4 units of an (n, H, W, 4) texel-quad view."""
-    if (quads.dtype != torch.float32 or quads.dim() != 4 or quads.shape[3] != 4 or quads.stride(3) != 1
-            or quads.stride(2) != 4 or quads.stride(0) % 4 or quads.stride(1) % 4):
-        raise ValueError("texel quads must be an (n, H, W, 4) float32 view with packed quads along W")
-    return quads.stride(0) // 4, quads.stride(1) // 4
+    """(layer, row) strides in element units of an (n, H, W, 4) texel-quad view,
+    or of an (n, H, W, 2) layer-pair view (sbrc quad_layout 1)."""
+    c = quads.shape[3] if quads.dim() == 4 else 0
+    if (quads.dtype != torch.float32 or quads.dim() != 4 or c not in (2, 4) or quads.stride(3) != 1
+            or quads.stride(2) != c or quads.stride(0) % c or quads.stride(1) % c):
+        raise ValueError("texel quads must be an (n, H, W, 4) (or layer pairs (n, H, W, 2)) float32 view "
+                         "packed along W")
+    return quads.stride(0) // c, quads.stride(1) // c
+
+
+def quad_layout(quads: torch.Tensor) -> int:
+    """0 = texel quads, 1 = layer pairs (sbrc_build_params.quad_layout)."""
+    return 1 if quads.shape[-1] == 2 else 0
 
 
 def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, quads: torch.Tensor,
@@ -286,6 +294,7 @@ def build_params(dvol: DeviceVolume, cam, spec, alpha_lut_dev, offsets_dev, quad
     else:
         qk, qy = quad_strides(quads)
     p = N.SbrcBuildParams()
+    p.quad_layout = 0 if plain else quad_layout(quads)
     p.volume = dvol.struct()
     p.light = light_frame(cam, spec, offsets_dev)
     p.alpha_lut = alpha_lut_dev.data_ptr()
@@ -372,6 +381,7 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
         if quads_dev is not None:
             p.quads = quads_dev.data_ptr()
             p.quad_layer_stride, p.quad_row_stride = quad_strides(quads_dev)
+            p.quad_layout = quad_layout(quads_dev)
         p.light_color[:] = [float(c) for c in np.asarray(light_color, dtype=np.float64)]
         p.ambient_floor = float(settings.ambient_floor)
     if mode in ("phong", "extinction"):

@@ -342,7 +342,10 @@ class FrameRenderer:
         self.offsets = f64_tensor(spec.plane_offsets, self.dev)
         n, h, w = int(spec.n_slices), int(light_cam.resolution[1]), int(light_cam.resolution[0])
         self._shape = (n, h, w)
-        self.storage = torch.empty((n, h, w, 4), dtype=torch.float32, device=self.dev)
+        # the hard-shadow march reads one lookup per sample: half-size layer pairs
+        # serve it faster than texel quads (profiles/r2_notes.md); the scattering modes keep quads
+        pairs = self.settings.shading_mode == "sbrc_shadow" and self.build_mode != "sharded" and w >= 2
+        self.storage = torch.empty((n, h, w, 2 if pairs else 4), dtype=torch.float32, device=self.dev)
         self.quads = self.storage
         if self.build_mode != "sharded" or self.world == 1:
             self.shard = None

@@ -58,3 +58,28 @@ def test_permute_rows_matches_index_select(torch):
     N.check(N.lib.sbrc_permute_rows(src.data_ptr(), p.data_ptr(), dst.data_ptr(), h, w, current_stream_handle()),
             "permute")
     assert torch.equal(dst, torch.index_select(src, 0, p))
+
+
+@pytest.mark.parametrize("case", ["blob32", "block48_u8", "config1"])
+def test_layer_pair_shadow_frames_identical(torch, case):
+    """FrameRenderer stores the stack as layer pairs (quad_layout 1) for the
+    one-lookup sbrc_shadow march; its frames equal the texel-quad path's bit
+    for bit (render_device + build_attenuation_buffer), and its intensity
+    view equals the reference's stack."""
+    from conftest import load_golden, scene_from_golden
+    import paper_2008_06134_b200 as sb
+    from paper_2008_06134_b200.frame import FramePipeline, FrameRenderer
+    g = load_golden(case)
+    v, tf, cam, spec, settings_for = scene_from_golden(g)
+    s = settings_for("sbrc_shadow")
+    ref = sb.render_device(v, tf, s, sb.build_attenuation_buffer(v, tf, cam, spec))
+    fr = FrameRenderer(v, tf, cam, spec, s)
+    assert fr.quads.shape[-1] == 2
+    assert torch.equal(fr.frame(), ref)
+    pipe = FramePipeline(fr)
+    for _ in range(3):
+        out = pipe.step()
+    pipe.drain()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    assert np.array_equal(fr.intensity.cpu().numpy(), g["intensity"])
