@@ -657,10 +657,13 @@ def run_ours(a, cfg, mode):
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["source"],
                 "algorithmic_bytes": d_bytes, "kernel_ms": d_ms,
                 "traffic": load_traffic(a.config, mode, dominant)}
-    roofline_k1 = {"bound": "hbm", "kernel": "build", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9,
-                   "peak": peaks["hbm_gbs"], "unit": "GB/s", "algorithmic_bytes": k1_bytes, "kernel_ms": k1_ms,
-                   "traffic": load_traffic(a.config, mode, "build")}
-    roofline_k1["frac"] = roofline_k1["achieved"] / peaks["hbm_gbs"]
+    if fr.needs_buffer:
+        roofline_k1 = {"bound": "hbm", "kernel": "build", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9,
+                       "peak": peaks["hbm_gbs"], "unit": "GB/s", "algorithmic_bytes": k1_bytes, "kernel_ms": k1_ms,
+                       "traffic": load_traffic(a.config, mode, "build")}
+        roofline_k1["frac"] = roofline_k1["achieved"] / peaks["hbm_gbs"]
+    else:  # none / phong / extinction read no attenuation stack: no K1 in the frame
+        roofline_k1 = None
     # Secondary view of K2: the bytes its gathers pull through L1/L2 per sample
     # (8 voxels + 2 16-byte texel quads per light lookup) against the SM-side
     # L1 data bandwidth (128 B/clk/SM at the max SM clock). The march is bound
@@ -699,8 +702,10 @@ def run_ours(a, cfg, mode):
             "samples_per_frame": samples,
             "march_only_fps": 1000.0 / (k2_ms + asm_ms),
             "kernels": {"build_ms": k1_ms, "march_ms": k2_ms, "assemble_ms": asm_ms,
-                        "build_gbs": k1_bytes / (k1_ms * 1e-3) / 1e9, "march_gbs": k2_bytes / (k2_ms * 1e-3) / 1e9,
-                        "build_gtexel_slices_s": cfg["n"] * cfg["res"] ** 2 / (k1_ms * 1e-3) / 1e9},
+                        "build_gbs": k1_bytes / (k1_ms * 1e-3) / 1e9 if fr.needs_buffer else None,
+                        "march_gbs": k2_bytes / (k2_ms * 1e-3) / 1e9,
+                        "build_gtexel_slices_s": cfg["n"] * cfg["res"] ** 2 / (k1_ms * 1e-3) / 1e9
+                        if fr.needs_buffer else None},
             "roofline": roofline,
             "roofline_build": roofline_k1,
             "roofline_l1": l1,

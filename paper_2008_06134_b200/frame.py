@@ -381,12 +381,23 @@ class FrameRenderer:
             self._complete = True
         return self.quads[..., 0]
 
+    @property
+    def needs_buffer(self) -> bool:
+        """Only the buffer modes read the attenuation stack (raycaster.py:395-411);
+        none / phong / extinction frames run no K1 (bench.render_scene builds
+        the buffer only for them too, bench.py:97-109)."""
+        return self.settings.shading_mode in ("sbrc_shadow", "shell", "cone")
+
     def build_into_buffer(self, quads: torch.Tensor) -> None:
         """This rank's K1 (replicated or frustum-culled) into ``quads``."""
+        if not self.needs_buffer:
+            return
         build_into(self.dvol, self.alpha, self.cam, self.spec, self.offsets, quads, self.comp, sparse=self.reach,
                    clip=self.clip)
 
     def build(self) -> None:
+        if not self.needs_buffer:
+            return
         if self.shard is None:
             self.build_into_buffer(self.quads)
             self._complete = self.reach is None
