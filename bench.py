@@ -751,6 +751,10 @@ def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
     h2d = 256 * 4 * 8 + 256 * 8 + n * 8
     d2h = cfg["image"] ** 2 * 16
 
+    host_img = None
+    if world > 1:  # page-locked landing buffer for the assembled image (one async D2H per frame)
+        host_img = torch.empty((cfg["image"], cfg["image"], 4), dtype=torch.float32).pin_memory()
+
     def step():
         if world == 1:
             buf = sb.build_attenuation_buffer(host_vol, tf, cam, spec)
@@ -759,7 +763,9 @@ def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
             fr.lut.copy_(torch.from_numpy(tf.resolve(settings.step)))
             fr.alpha.copy_(torch.from_numpy(np.ascontiguousarray(tf.resolve(spec.spacing)[:, 3])))
             fr.offsets.copy_(torch.from_numpy(spec.plane_offsets))
-            img = fr.frame().cpu().numpy()
+            host_img.copy_(fr.frame(), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            img = host_img.numpy()
         return img
 
     for _ in range(3):
