@@ -497,12 +497,14 @@ class FramePipeline:
     throughout when one GPU's share of the image is small), which the next
     build fills."""
 
-    def __init__(self, fr: FrameRenderer):
+    def __init__(self, fr: FrameRenderer, build_priority: int = 0):
         if fr.shard is not None:
             raise ValueError("pipelining needs the replicated build")
         self.fr = fr
         self.bufs = [fr.quads, torch.empty_like(fr.quads)]
-        self.build_stream = torch.cuda.Stream(fr.dev)
+        # build_priority: CUDA stream priority of the build stream (0 = default; higher-priority
+        # launches get their blocks dispatched first when both kernels have blocks pending)
+        self.build_stream = torch.cuda.Stream(fr.dev, priority=build_priority)
         self.built = [torch.cuda.Event(), torch.cuda.Event()]
         self.released = [torch.cuda.Event(), torch.cuda.Event()]
         self.f = 0
