@@ -713,7 +713,10 @@ def run_ours(a, cfg, mode):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_full_frame_config2": full2,
-            "gpu_launches": 2 * a.steps,
+            # per frame: K1 (if the mode reads a buffer) + K2, plus the measured
+            # heavy-first sort (sbrc_tile_order) and the NCCL assembly's row permutation at N > 1
+            "gpu_launches": a.steps * (int(fr.needs_buffer) + 1 + int(fr.feedback is not None)
+                                       + int(world > 1 and fr.assemble_mode == "nccl")),
             "clocks": clocks.summary(),
             "volume_gen_s": vol_gen_s,
         }
