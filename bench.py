@@ -530,7 +530,21 @@ def run_ours(a, cfg, mode):
 
     tf, cam, spec, settings = scene_objects(cfg, mode)
     t0 = time.perf_counter()
-    dvol, host_vol = device_volume_for(cfg, dev)
+    bcast_ms = None
+    if world > 1:
+        # rank 0 makes the dataset, one broadcast replicates it, timed on its own
+        from paper_2008_06134_b200.device import broadcast_volume
+        dvol, host_vol = device_volume_for(cfg, dev) if rank == 0 else (None, None)
+        d = cfg["dims"]
+        vt = {"blobs": 0, "block_u8": 1, "blobs_u16": 2}[cfg["volume"]]
+        torch.cuda.synchronize()
+        dist.barrier()
+        tb = time.perf_counter()
+        dvol = broadcast_volume(dvol, (d, d, d), vt, np.zeros(3), np.ones(3), dev)
+        torch.cuda.synchronize()
+        bcast_ms = (time.perf_counter() - tb) * 1e3
+    else:
+        dvol, host_vol = device_volume_for(cfg, dev)
     if not a.raw_voxels:
         dvol = dvol.widened()
     torch.cuda.synchronize()
@@ -719,6 +733,7 @@ def run_ours(a, cfg, mode):
                                        + int(world > 1 and fr.assemble_mode == "nccl")),
             "clocks": clocks.summary(),
             "volume_gen_s": vol_gen_s,
+            "volume_broadcast_ms": bcast_ms,
         }
         print(json.dumps(line), flush=True)
     fr.close()

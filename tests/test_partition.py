@@ -156,3 +156,36 @@ def test_recut_collective_gloo(world):
     cuts = {tuple(map(tuple, new)) for _, new, _ in res}
     assert len(cuts) == 1
     assert list(cuts)[0] == tuple(map(tuple, res[0][2]))
+
+
+def _bcast_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2008_06134_b200 import _native as N
+    from paper_2008_06134_b200.device import DeviceVolume, broadcast_volume
+    dims = (6, 5, 4)
+    src = None
+    if rank == 0:
+        t = (torch.arange(4 * 5 * 6, dtype=torch.int32) * 517 % 65536).to(torch.int16).view(4, 5, 6)
+        src = DeviceVolume(t, N.VOXEL_U16, dims, np.zeros(3), np.ones(3))
+    got = broadcast_volume(src, dims, N.VOXEL_U16, np.zeros(3), np.ones(3), "cpu")
+    want = (torch.arange(4 * 5 * 6, dtype=torch.int32) * 517 % 65536).to(torch.int16).view(4, 5, 6)
+    q.put((rank, bool(torch.equal(got.data, want)), got.voxel_type, got.dims))
+    dist.destroy_process_group()
+
+
+def test_broadcast_volume_gloo():
+    """device.broadcast_volume: every rank ends with rank 0's voxels, type and dims."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok and vt == 2 and dims == (6, 5, 4) for _, ok, vt, dims in res), res
