@@ -566,25 +566,8 @@ def run_ours(a, cfg, mode):
         samples = int(t.item())
 
     if world > 1 and a.build == "frustum":
-        # contiguous bands re-cut from measured per-rank frame times (FrameRenderer.rebalance)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        best = None
-        for _ in range(6):
-            fr.choose_march_kernel()  # throughput or latency K2 for this rank's band, by measurement
-            ev[0].record(stream)
-            for _ in range(3):
-                fr.build()
-                fr.march(count_samples=False)
-            ev[1].record(stream)
-            torch.cuda.synchronize()
-            t = torch.tensor([ev[0].elapsed_time(ev[1]) / 3], dtype=torch.float64, device=dev)
-            worst = t.clone()
-            dist.all_reduce(worst, op=dist.ReduceOp.MAX)
-            if best is None or worst.item() < best[0]:
-                best = (worst.item(), list(fr.ranges), fr.march_kernel)
-            fr.rebalance(t.item())
-        fr.set_ranges(best[1])
-        fr.march_kernel = best[2]
+        # contiguous bands cut from measured per-rank frame times, each rank's K2 kernel measured too
+        fr.calibrate()
         fr.frame()
     pipelined = (world == 1 or a.build in ("replicated", "frustum")) and not a.no_pipeline
     pipe = FramePipeline(fr) if pipelined else None

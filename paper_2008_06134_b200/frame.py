@@ -228,6 +228,50 @@ class FrameRenderer:
         self.set_ranges(PT.damped_ranges(self.ranges, PT.balanced_ranges(prof, self.world), self.height))
         return self.ranges
 
+    def _frame_times(self, frames: int) -> list:
+        """Every rank's device time of `frames` build + march frames (ms per
+        frame), exchanged with one all-reduce."""
+        stream = torch.cuda.current_stream(self.dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(frames):
+            self.build()
+            self.march(False)
+        e1.record(stream)
+        e1.synchronize()
+        mine = e0.elapsed_time(e1) / frames
+        if self.world == 1:
+            return [mine]
+        nccl = dist.get_backend(self.group) == "nccl"
+        t = torch.zeros(self.world, dtype=torch.float64, device=self.dev if nccl else "cpu")
+        t[self.rank] = mine
+        dist.all_reduce(t, group=self.group)
+        return t.cpu().tolist()
+
+    def calibrate(self, iters: int = 10, frames: int = 3) -> list:
+        """Contiguous partition: each round every rank picks its K2 kernel for
+        its band (choose_march_kernel) and the bands are timed; the next cut
+        steps from the best cut seen so far (its times spread over the bands
+        like the geometric row profile, re-balanced, boundaries moved halfway:
+        partition.calibrated_profile / balanced_ranges / damped_ranges), so
+        timing noise cannot walk the cut away from a good one. Ends on the
+        best cut and each rank's kernel for it. Collective; returns the cut."""
+        shape = PT.row_costs_geometric(self.settings)
+        best = None
+        for _ in range(iters):
+            self.choose_march_kernel()
+            times = self._frame_times(frames)
+            if best is None or max(times) < best[0]:
+                best = (max(times), list(self.ranges), self.march_kernel, times)
+            nxt = PT.damped_ranges(best[1], PT.balanced_ranges(PT.calibrated_profile(shape, best[1], best[3]),
+                                                                self.world), self.height)
+            if nxt == list(self.ranges):  # converged (every rank computes the same cut)
+                break
+            self.set_ranges(nxt)
+        self.set_ranges(best[1])
+        self.march_kernel = best[2]
+        return self.ranges
+
     def choose_march_kernel(self, frames: int = 3) -> int:
         """Time this rank's march with the throughput and the latency K2
         kernel (CUDA events, after one warm-up each) and keep the faster —

@@ -61,20 +61,24 @@ def main():
         ranges = PT.balanced_ranges(shape, world)
         history = []
         kernels = [0] * world
-        for _ in range(6 if world > 1 else 0):  # re-cut by measured per-rank frame times
+        best = None
+        for _ in range(10 if world > 1 else 0):  # FrameRenderer.calibrate's search, ranks one after the other
             times = []
             for r in range(world):
                 fr = rank_renderer(dvol, scene, world, r, ranges)
-                if world > 1:
-                    kernels[r] = fr.choose_march_kernel()
+                kernels[r] = fr.choose_march_kernel()
                 times.append(timed(lambda: (fr.build(), fr.march(False)), k=5))
                 del fr
                 gc.collect()
             history.append({"ranges": ranges, "max_ms": max(times), "times": times, "kernels": list(kernels)})
-            ranges = PT.damped_ranges(ranges, PT.balanced_ranges(PT.calibrated_profile(shape, ranges, times), world),
-                                      settings.viewport[1])
-        if history:  # the best cut seen, with the kernels each rank chose for it
-            best = min(history, key=lambda e: e["max_ms"])
+            if best is None or max(times) < best["max_ms"]:
+                best = history[-1]
+            nxt = PT.damped_ranges(best["ranges"], PT.balanced_ranges(
+                PT.calibrated_profile(shape, best["ranges"], best["times"]), world), settings.viewport[1])
+            if nxt == ranges:
+                break
+            ranges = nxt
+        if best is not None:  # the best cut seen, with the kernels each rank chose for it
             ranges, kernels = best["ranges"], best["kernels"]
         ranks = []
         same = True
