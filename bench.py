@@ -973,6 +973,9 @@ def main():
     if a.impl == "reference":
         return run_reference(a, cfg, mode)
     if a.config == 5:
+        # the sweep is a single-GPU measurement: under torchrun rank 0 runs it, the others exit
+        if int(os.environ.get("RANK", "0")) != 0:
+            return 0
         return run_sweep(a, cfg, mode)
     return run_ours(a, cfg, mode)
 
