@@ -28,11 +28,25 @@
 // would break 1e-3.
 //
 // Performance notes (profiles/). The march is issue-bound,
-// not HBM-bound (L1 hit rate ~98%): the design minimises instructions per
+// not HBM-bound (L1 hit rate 94%): the design minimises instructions per
 // sample — texel quads turn a two-layer bilinear lookup into two 16-byte
 // loads, offsets are 32-bit, edge clamping is folded into saturated
 // weights, the trilinear fetch has an unclamped interior fast path, and the
 // default cone (2 x 4) and shell (3 shells) kernels are unrolled.
+//
+// Measured alternatives kept as build switches (default off unless noted;
+// numbers: config 3 on one B200, profiles/r2_notes.md):
+//   SBRC_PACKED        FFMA2/FADD2 shell taps: ON (shell 4.92 -> 4.73 ms)
+//   SBRC_PACKED_CONE   the same for cone taps (2.87 -> 3.17-3.20 ms)
+//   SBRC_WARP_VOTE     __any_sync march loop (2.87 -> 3.43 ms)
+//   SBRC_PREC          float32 colour / sample paths (2.84 / 2.60 ms, the
+//                      latter 1.2e-3 over the contract on 3 pixels)
+//   SBRC_PAIRS         layer-pair stack for every mode (cone 3.01, shell
+//                      5.63, shadow 1.45 ms) — pairs are chosen at run time
+//                      for sbrc_shadow frames instead (quad_layout)
+//   SBRC_BRICK         8^3-cell bricks with apron (K2 2.96, K1 0.37 ms)
+//   SBRC_BUILD_ASYNC   K1 cp.async gather pipeline (sbrc.cu; 0.36 ms at D=4)
+//   SBRC_BUILD_TMA     K1 TMA-staged volume boxes (sbrc.cu; 1.02 ms)
 
 #include "../../include/sbrc.h"
 
