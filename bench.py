@@ -329,13 +329,19 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU sample
-def cpu_sample_plan(cfg):
+def cpu_sample_plan(cfg, workers: int = 1):
     """Bounded, stratified sample of one frame for the CPU path: every 16th light
-    row for the build, rows/cols 6::12 of the image for the march."""
+    row for the build, full-width image rows for the march — every 16th on one
+    core, and on `workers` cores enough rows for 16 per worker. The oracle's
+    numpy march has a fixed cost per call and per step, so each worker must get
+    as many rays per call as on a whole frame for the extrapolation by row
+    count to match a measured full frame (a sparse 85x85 pixel grid overstated
+    the CPU frame ~6x, 4 rows per worker ~1.7x: r4f-r4h)."""
     res, img = cfg["res"], cfg["image"]
-    b_rows = np.arange(8, res, 16) if res >= 32 else np.arange(res)
-    stride = 12 if img >= 256 else 1
-    p_rows = np.arange(6, img, stride) if stride > 1 else np.arange(img)
+    bstride = 16 if workers <= 1 else max(1, res // (16 * workers))
+    b_rows = np.arange(bstride // 2, res, bstride) if res >= 32 else np.arange(res)
+    stride = 16 if workers <= 1 else max(1, img // (16 * workers))
+    p_rows = np.arange(stride // 2, img, stride) if img >= 256 else np.arange(img)
     return b_rows, p_rows
 
 
@@ -373,34 +379,46 @@ def _cpu_march_part(args):
 def cpu_frame_sample(cfg, workers=1, pool=None):
     """Time the oracle on the bounded sample of one frame; extrapolate to the
     full frame. Returns (frame_seconds, detail, (build_rows_out, march_pixels_out))."""
-    b_rows, p_rows = cpu_sample_plan(cfg)
+    b_rows, p_rows = cpu_sample_plan(cfg, workers if pool is not None else 1)
     t0 = time.perf_counter()
     if pool is None:
         built = [_cpu_build_part((b_rows,))[1]]
     else:
-        built = [o for _, o in pool.map(_cpu_build_part, [(c,) for c in np.array_split(b_rows, workers) if len(c)])]
+        bparts = [b_rows[i::workers] for i in range(workers) if len(b_rows[i::workers])]
+        built = [o for _, o in pool.map(_cpu_build_part, [(c,) for c in bparts])]
+        border = np.argsort(np.concatenate([np.arange(len(b_rows))[i::workers] for i in range(workers)
+                                            if len(b_rows[i::workers])]), kind="stable")
+        built = [np.concatenate(built, axis=1)[:, border]]
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
+    cols = np.arange(cfg["image"])
     if pool is None:
-        parts = [_cpu_march_part((p_rows, p_rows))]
+        parts = [_cpu_march_part((p_rows, cols))]
     else:
-        parts = list(pool.map(_cpu_march_part, [(r, p_rows) for r in np.array_split(p_rows, workers) if len(r)]))
+        # rows dealt round-robin: every worker gets rows from the whole image (balanced cost)
+        parts = list(pool.map(_cpu_march_part, [(p_rows[i::workers], cols) for i in range(workers)
+                                                if len(p_rows[i::workers])]))
     t_march = time.perf_counter() - t0
     samples = sum(n for _, n, _ in parts)
     full_build = t_build * cfg["res"] / len(b_rows)
-    full_march = t_march * cfg["image"] ** 2 / (len(p_rows) ** 2)
-    detail = dict(build_rows=int(len(b_rows)), march_pixels=int(len(p_rows) ** 2), march_samples=int(samples),
-                  build_fraction=len(b_rows) / cfg["res"], march_fraction=len(p_rows) ** 2 / cfg["image"] ** 2,
+    full_march = t_march * cfg["image"] / len(p_rows)
+    detail = dict(build_rows=int(len(b_rows)), march_pixels=int(len(p_rows) * cfg["image"]), march_samples=int(samples),
+                  build_fraction=len(b_rows) / cfg["res"], march_fraction=len(p_rows) / cfg["image"],
                   t_build_s=t_build, t_march_s=t_march, build_s_extrapolated=full_build,
                   march_s_extrapolated=full_march, extrapolated=True)
-    outputs = (np.concatenate(built, axis=1), np.concatenate([im for _, _, im in parts], axis=0))
+    march = np.concatenate([im for _, _, im in parts], axis=0)
+    if pool is not None:  # back to p_rows order (rows were dealt round-robin)
+        order = np.concatenate([np.arange(len(p_rows))[i::workers] for i in range(workers)
+                                if len(p_rows[i::workers])])
+        march = march[np.argsort(order, kind="stable")]
+    outputs = (np.concatenate(built, axis=1), march)
     return full_build + full_march, detail, outputs
 
 
-def cpu_sample_text(cfg):
-    b_rows, p_rows = cpu_sample_plan(cfg)
+def cpu_sample_text(cfg, workers: int = 1):
+    b_rows, p_rows = cpu_sample_plan(cfg, workers)
     return (f"oracle (numpy port of the reference) on a stratified sample of one frame: build on "
-            f"{len(b_rows)}/{cfg['res']} light rows, march on {len(p_rows)}x{len(p_rows)} of "
+            f"{len(b_rows)}/{cfg['res']} light rows, march on {len(p_rows)} full-width rows ({len(p_rows)}x{cfg['image']}) of "
             f"{cfg['image']}x{cfg['image']} pixels; frame time extrapolated by row/pixel count")
 
 
@@ -429,11 +447,12 @@ def _full_build(pool, workers, res):
     return np.concatenate([o for _, o in parts], axis=1)
 
 
-def reference_full_frame(workers, ctx):
-    """One complete, unextrapolated config-2 frame of the reference CPU path
-    (build on all light rows, march on every pixel) on all host cores."""
-    cfg = CONFIGS[2]
-    vol, tf, cam, spec, settings = oracle_scene(cfg, cfg["mode"])
+def reference_full_frame(workers, ctx, cfg_id: int = 2, mode: str | None = None, scene=None):
+    """One complete, unextrapolated frame of the reference CPU path (build on
+    all light rows, march on every pixel, 4 row bands per core for balance)
+    on all host cores. ``scene`` reuses already generated oracle inputs."""
+    cfg = CONFIGS[cfg_id]
+    vol, tf, cam, spec, settings = scene if scene is not None else oracle_scene(cfg, mode or cfg["mode"])
     set_cpu_context(vol, tf, cam, spec, settings, None)
     with ctx.Pool(workers) as pool:
         t0 = time.perf_counter()
@@ -443,10 +462,10 @@ def reference_full_frame(workers, ctx):
     with ctx.Pool(workers) as pool:  # forked after the stack exists
         t0 = time.perf_counter()
         rows = np.arange(cfg["image"])
-        parts = pool.map(_cpu_march_part, [(r, rows) for r in np.array_split(rows, workers) if len(r)])
+        parts = pool.map(_cpu_march_part, [(r, rows) for r in np.array_split(rows, 4 * workers) if len(r)])
         t_march = time.perf_counter() - t0
     frame = t_build + t_march
-    return {"config": f"config 2: {cfg['name']}", "fps": 1.0 / frame, "frame_s": frame, "build_s": t_build,
+    return {"config": f"config {cfg_id}: {cfg['name']}", "fps": 1.0 / frame, "frame_s": frame, "build_s": t_build,
             "march_s": t_march, "samples": int(sum(n for _, n, _ in parts)), "cores": workers,
             "extrapolated": False}
 
@@ -483,6 +502,9 @@ def run_reference(a, cfg, mode):
     frame_s = statistics.median(times)
     fps = 1.0 / frame_s
     full = None if a.no_full_frame else reference_full_frame(workers, ctx)
+    # the benchmarked workload itself, complete and unextrapolated (config 3: ~20 s on 16 cores)
+    full_cfg = None if (a.no_full_frame or a.config not in (1, 3)) else \
+        reference_full_frame(workers, ctx, a.config, mode, scene=(vol, tf, cam, spec, settings))
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
@@ -494,8 +516,9 @@ def run_reference(a, cfg, mode):
         "sample_ms_per_step": statistics.median(walls) * 1e3,
         "gsamples_per_s": detail["march_samples"] / max(detail["t_march_s"], 1e-12) / 1e9,
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": "port",
-                         "sample": cpu_sample_text(cfg), "cpu_model": host["model"], "detail": detail},
+                         "sample": cpu_sample_text(cfg, workers), "cpu_model": host["model"], "detail": detail},
         "full_frame_config2": full,
+        "full_frame": full_cfg,
         "product_package_loaded": any(m.split(".")[0] == "paper_2008_06134_b200" for m in sys.modules),
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -806,12 +829,12 @@ def cpu_baseline_leg(cfg, tf, cam, spec, settings, dvol, host_vol, intensity, im
     set_cpu_context(host_vol, tf, cam, spec, settings, intensity)
     frame_s, detail, (rows_cpu, pix_cpu) = cpu_frame_sample(cfg)
     b_rows, p_rows = cpu_sample_plan(cfg)
-    parity = {"rows": int(len(b_rows)), "pixels": int(len(p_rows) ** 2), "tolerance": 1e-3}
+    parity = {"rows": int(len(b_rows)), "pixels": int(len(p_rows) * cfg["image"]), "tolerance": 1e-3}
     if intensity is not None:
         got = intensity[:, b_rows]
         parity["build_rows_bit_exact"] = bool(np.array_equal(got, rows_cpu))
         parity["build_max_abs"] = float(np.abs(got.astype(np.float64) - rows_cpu).max())
-    got = image[np.ix_(p_rows, p_rows)].astype(np.float64)
+    got = image[p_rows].astype(np.float64)
     d = np.abs(got - pix_cpu.astype(np.float64))
     mse = float(np.mean(d * d))
     parity.update(max_abs=float(d.max()), psnr=float("inf") if mse == 0 else 10.0 * math.log10(1.0 / mse),
