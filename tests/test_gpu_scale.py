@@ -1,8 +1,9 @@
 """Parity at BASELINE.json's full sizes (configs 2, 3, 4). Needs a B200.
 
-The oracle cannot render a 1024^2 cone frame in test time (~6 CPU-minutes per
-frame at config 3), so full-size frames are checked three ways:
+Full-size frames are checked four ways (the oracle renders a whole 1024^2
+cone frame in ~20 s on the box's 16 cores):
 
+- every pixel against the oracle (configs 1, 2 and 3, test_every_pixel_vs_oracle);
 - against the oracle on a stratified subset: light-texel rows of the build
   (bit-exact) and image pixels of the march (<= 1e-4), the march subset
   reading the GPU-built stack (itself bit-exact on the checked rows);
@@ -135,3 +136,39 @@ def test_config4_full_size(sb):
     del raw
     _check_full_frame(sb, v, cfg, tf, cam, spec, settings, build_rows=np.arange(8, 1024, 16),
                       pix=np.arange(8, 2048, 16), gpu_vol=dvol)
+
+
+@pytest.mark.parametrize("cfg_id,mode", [(1, "shell"), (2, "sbrc_shadow"), (3, "none"), (3, "cone")])
+def test_every_pixel_vs_oracle(sb, cfg_id, mode):
+    """Whole frames, every pixel, against the oracle (its march forked over all
+    host cores, reading the GPU-built stack; ~20 s for config 3's cone frame on
+    16 cores): config 1 shell, config 2 hard shadow and config 3 cone (the
+    headline, 1,048,576 pixels) within 1e-4 with equal executed-sample counts,
+    config 3's float64 `none` image bit-identical."""
+    import multiprocessing as mp
+    import torch
+    import bench
+    from paper_2008_06134_b200.frame import FrameRenderer
+    from paper_2008_06134_b200.scene import VolumeDataset
+    cfg, tf, cam, spec, settings = _scene(cfg_id, mode)
+    dvol, _ = bench.device_volume_for(cfg, torch.device("cuda"))
+    dvol = dvol.widened()
+    fr = FrameRenderer(dvol, tf, cam, spec, settings)
+    fr.reset_counter()
+    img = fr.frame().cpu().numpy()
+    gpu_samples = int(fr.counter.item())
+    inten = fr.intensity.contiguous().cpu().numpy() if fr.needs_buffer else None
+    host = VolumeDataset.from_array(dvol.data.cpu().numpy())
+    bench.set_cpu_context(host, tf, cam, spec, settings, inten)
+    rows, cols = np.arange(cfg["image"]), np.arange(cfg["image"])
+    workers = max(1, len(os.sched_getaffinity(0)))
+    with mp.get_context("fork").Pool(workers) as pool:
+        parts = pool.map(bench._cpu_march_part, [(r, cols) for r in np.array_split(rows, 4 * workers) if len(r)])
+    want = np.concatenate([im for _, _, im in parts], axis=0)
+    assert gpu_samples == sum(n for _, n, _ in parts)
+    if mode == "none":
+        assert np.array_equal(img, want)
+    else:
+        st = parity_stats(img, want)
+        print(f"[every pixel] config {cfg_id} {mode}: max_abs={st['max_abs']:.2e} psnr={st['psnr']:.1f}")
+        assert st["max_abs"] <= 1e-4, st
