@@ -4,7 +4,7 @@ parallelised over row bands on all host cores, reading the GPU-built
 attenuation stack (itself checked bit-exact on sampled light rows here and
 in every bench run). Test infrastructure, like the bench's CPU legs.
 
-    python scripts/full_parity.py [config ...] [--mode M]    (default: 1 2 3)
+    python scripts/full_parity.py [config ...] [--mode M]    (default: 1 2 3; 5 = one orbit-light frame)
 
 Prints one JSON line per (config, mode): max-abs, PSNR, pixels over 1e-3 /
 1e-4, whether the image is bit-identical, executed samples GPU vs oracle.
@@ -36,6 +36,11 @@ def main():
         cfg = bench.CONFIGS[cid]
         mode = mode_arg or cfg["mode"]
         tf, cam, spec, settings = bench.scene_objects(cfg, mode)
+        if cid == 5:  # one moving-light frame of the sweep: orbit light az 135, el 30 (orbit.ts:28-35)
+            from paper_2008_06134_b200 import scene
+            ld = bench.orbit_light(135.0, 30.0)
+            cam = scene.LightCamera.fit(ld, (1.0, 1.0, 1.0), (cfg["res"], cfg["res"]))
+            spec = scene.make_slice_stack(ld, cfg["n"])
         dvol, _ = bench.device_volume_for(cfg, dev)
         dvol = dvol.widened()
         fr = FrameRenderer(dvol, tf, cam, spec, settings, device=dev)
