@@ -541,7 +541,7 @@ class FramePipeline:
     throughout when one GPU's share of the image is small), which the next
     build fills."""
 
-    def __init__(self, fr: FrameRenderer, build_priority: int = 0):
+    def __init__(self, fr: FrameRenderer, build_priority: int = 0, build_after_march: bool = False):
         if fr.shard is not None:
             raise ValueError("pipelining needs the replicated build")
         self.fr = fr
@@ -549,6 +549,9 @@ class FramePipeline:
         # build_priority: CUDA stream priority of the build stream (0 = default; higher-priority
         # launches get their blocks dispatched first when both kernels have blocks pending)
         self.build_stream = torch.cuda.Stream(fr.dev, priority=build_priority)
+        # launch order of one step: the next frame's build before this march (its
+        # blocks are dispatched first) or after it (it fills the march's tail)
+        self.build_after_march = build_after_march
         self.built = [torch.cuda.Event(), torch.cuda.Event()]
         self.released = [torch.cuda.Event(), torch.cuda.Event()]
         self.f = 0
@@ -565,7 +568,8 @@ class FramePipeline:
         fr, i = self.fr, self.f % 2
         if self.pending is None:
             self._launch_build(i)
-        self._launch_build(1 - i)  # next frame's stack, overlapping this march
+        if not self.build_after_march:
+            self._launch_build(1 - i)  # next frame's stack, overlapping this march
         self.pending = 1 - i
         main = torch.cuda.current_stream(fr.dev)
         main.wait_event(self.built[i])
@@ -573,6 +577,8 @@ class FramePipeline:
         fr._complete = fr.reach is None
         fr.march(count_samples)
         self.released[i].record(main)
+        if self.build_after_march:
+            self._launch_build(1 - i)
         img = fr.assemble()
         self.f += 1
         return img
