@@ -469,11 +469,60 @@ __global__ void __launch_bounds__(32 * SBRC_BUILD_ROWS,
       prev = st;
     }
   } else {
+  // Interior segment [kS, kE]: slices at which every lane's point lies inside
+  // the volume with its whole trilinear cell (the texel line's interval in the
+  // cube shrunk by half a voxel plus 1e-9 per face, one slice of slack each
+  // side) — there the float64 cube test and the clamped-cell branch are
+  // certainly true / untaken and are skipped (same values, bit-identical).
+  int kS = n, kE = -1;
+  if constexpr (UNIT && D == 0) {
+    if (SBRC_BUILD_FASTSEG) {
+      const int dims[3] = {P.volume.nx, P.volume.ny, P.volume.nz};
+      const double spacing = (L.d_max - L.d_min) / n;
+      double ilo = -INFINITY, ihi = INFINITY;
+      bool ok = row_ok;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double lc = L.light_dir[c];
+        const double m_lo = 0.5 / dims[c] + 1e-9, m_hi = (dims[c] - 0.5) / dims[c] - 1e-9;
+        if (fabs(lc) < 1e-6) {
+          ok = false;
+        } else {
+          const double a = (m_lo - base[c]) / lc, b = (m_hi - base[c]) / lc;
+          ilo = fmax(ilo, fmin(a, b));
+          ihi = fmin(ihi, fmax(a, b));
+        }
+      }
+      int i_lo = n, i_hi = -1;
+      if (ok && ilo < ihi) {
+        i_lo = max(0, (int)ceil((ilo - L.d_min) / spacing - 0.5) + 1);
+        i_hi = min(n - 1, (int)floor((ihi - L.d_min) / spacing - 0.5) - 1);
+      }
+      kS = __reduce_max_sync(0xffffffffu, i_lo <= i_hi ? i_lo : n);
+      kE = __reduce_min_sync(0xffffffffu, i_lo <= i_hi ? i_hi : -1);
+      kS = max(kS, kA);
+      kE = min(kE, kB);
+    }
+  }
+  auto fast_slice = [&](int kk) {
+    double px, py, pz;
+    point(kk, px, py, pz);
+    Cell<VT> cl;
+    cell_fetch_interior<VT>(P.volume, px, py, pz, cl);
+    const float st = step_slice(true, cl);
+    if (kk > 0) emit_w(kk - 1, prev, st);
+    prev = st;
+  };
   // SBRC_BUILD_UNROLL slices at a time: the gathers of all of them are issued
   // before any is combined (the product order of T is unchanged, so the
   // result stays bit-exact).
   constexpr int U = SBRC_BUILD_UNROLL;
   for (; k + U <= kB + 1; k += U) {
+    if (k >= kS && k <= kE) {  // warp-uniform: the interior segment, one slice at a time
+      for (; k <= kE; ++k) fast_slice(k);
+      k -= U;  // (the loop increment)
+      continue;
+    }
     bool cov[U];
     Cell<VT> cl[U];
 #pragma unroll

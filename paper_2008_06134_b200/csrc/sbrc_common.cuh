@@ -79,6 +79,9 @@
 #ifndef SBRC_CONE_RING_SERIAL
 #define SBRC_CONE_RING_SERIAL 0  // 1: one cone ring's loads in flight at a time (fewer registers)
 #endif
+#ifndef SBRC_BUILD_FASTSEG
+#define SBRC_BUILD_FASTSEG 1  // K1: slices where the whole warp is inside the volume skip the cube/face tests
+#endif
 #ifndef SBRC_BUILD_UNROLL
 #define SBRC_BUILD_UNROLL 1  // slices whose gathers are issued together in K1 (1 + 8 blocks/SM: -3%, r3h)
 #endif
@@ -263,6 +266,32 @@ __device__ __forceinline__ void cell_fetch(const sbrc_volume& v, double px, doub
     cl.r[4] = __ldg(base + (z1 + y0 + a[0])); cl.r[5] = __ldg(base + (z1 + y0 + b[0]));
     cl.r[6] = __ldg(base + (z1 + y1 + a[0])); cl.r[7] = __ldg(base + (z1 + y1 + b[0]));
   }
+}
+
+// cell_fetch for a point known to be inside the unit-box volume with its
+// whole cell (lo in [0, n-2] on every axis): no clamps, no bounds tests.
+template <int VT>
+__device__ __forceinline__ void cell_fetch_interior(const sbrc_volume& v, double px, double py, double pz,
+                                                    Cell<VT>& cl) {
+  using T = typename Voxel<VT>::T;
+  const double p[3] = {px, py, pz};
+  const int dims[3] = {v.nx, v.ny, v.nz};
+  int lo[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double g = dsub(dmul(p[c], (double)dims[c]), 0.5);
+    const FloorD fl = floor_d(g);
+    cl.f[c] = dsub(g, fl.f);
+    lo[c] = fl.i;
+  }
+  const unsigned nx = (unsigned)v.nx, nxy = (unsigned)v.nx * (unsigned)v.ny;
+  const T* c = reinterpret_cast<const T*>(v.data) + ((unsigned)lo[0] + nx * (unsigned)lo[1] + nxy * (unsigned)lo[2]);
+  SBRC_CHECK(lo[0] >= 0 && lo[1] >= 0 && lo[2] >= 0 && lo[0] < v.nx - 1 && lo[1] < v.ny - 1 && lo[2] < v.nz - 1, 0);
+  const T* cy = c + nx;
+  const T* cz = c + nxy;
+  const T* cyz = cz + nx;
+  cl.r[0] = __ldg(c); cl.r[1] = __ldg(c + 1); cl.r[2] = __ldg(cy); cl.r[3] = __ldg(cy + 1);
+  cl.r[4] = __ldg(cz); cl.r[5] = __ldg(cz + 1); cl.r[6] = __ldg(cyz); cl.r[7] = __ldg(cyz + 1);
 }
 
 template <int VT>
