@@ -79,6 +79,9 @@
 #ifndef SBRC_CONE_RING_SERIAL
 #define SBRC_CONE_RING_SERIAL 0  // 1: one cone ring's loads in flight at a time (fewer registers)
 #endif
+#ifndef SBRC_MARCH_FASTSEG
+#define SBRC_MARCH_FASTSEG 1  // K2: samples inside the ray's interior t-range skip the cube/face tests
+#endif
 #ifndef SBRC_BUILD_FASTSEG
 #define SBRC_BUILD_FASTSEG 1  // K1: slices where the whole warp is inside the volume skip the cube/face tests
 #endif
@@ -826,6 +829,30 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       t_far = fmin(t_far, fmax(lo, hi));
     }
     const double t_enter = fmax(t_near, 0.0);
+    // Interior t-range of the ray (unit box): samples whose position lies half
+    // a voxel + 1e-9 inside every face are in the cube with their whole cell,
+    // so the march skips the float64 cube test and the clamped-cell branch
+    // there (the same values; SBRC_MARCH_FASTSEG).
+    double t_safe_lo = INFINITY, t_safe_hi = -INFINITY;
+    if constexpr (UNIT && SBRC_MARCH_FASTSEG) {
+      const int vd[3] = {P.volume.nx, P.volume.ny, P.volume.nz};
+      double lo_t = -INFINITY, hi_t = INFINITY;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double m_lo = 0.5 / vd[c] + 1e-9, m_hi = (vd[c] - 0.5) / vd[c] - 1e-9;
+        if (fabs(d[c]) < 1e-12) {
+          if (!(P.eye[c] > m_lo && P.eye[c] < m_hi)) hi_t = -INFINITY;
+        } else {
+          const double a = (m_lo - P.eye[c]) / d[c], b = (m_hi - P.eye[c]) / d[c];
+          lo_t = fmax(lo_t, fmin(a, b));
+          hi_t = fmin(hi_t, fmax(a, b));
+        }
+      }
+      if (lo_t < hi_t) {
+        t_safe_lo = lo_t;
+        t_safe_hi = hi_t;
+      }
+    }
 
     if (t_far > t_enter) {
       QuadTex tex;
@@ -1069,8 +1096,13 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
           const double qx = dadd(P.eye[0], dmul(tn, d[0]));
           const double qy = dadd(P.eye[1], dmul(tn, d[1]));
           const double qz = dadd(P.eye[2], dmul(tn, d[2]));
-          fill_in = in_cube(qx, qy, qz);
-          if (fill_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, fill);
+          if (UNIT && SBRC_MARCH_FASTSEG && tn >= t_safe_lo && tn <= t_safe_hi) {
+            fill_in = true;
+            cell_fetch_interior<VT>(P.volume, qx, qy, qz, fill);
+          } else {
+            fill_in = in_cube(qx, qy, qz);
+            if (fill_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, fill);
+          }
         }
 #if SBRC_PREC == 0
         const double s = use_in ? cell_combine<VT>(use, reinterpret_cast<const float*>(u8tab)) : 0.0;
