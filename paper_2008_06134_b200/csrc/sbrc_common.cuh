@@ -79,6 +79,9 @@
 #ifndef SBRC_CONE_RING_SERIAL
 #define SBRC_CONE_RING_SERIAL 0  // 1: one cone ring's loads in flight at a time (fewer registers)
 #endif
+#ifndef SBRC_LIGHT_FASTSEG
+#define SBRC_LIGHT_FASTSEG 1  // K2: the clamp-free light-lookup samples as one counter interval per ray
+#endif
 #ifndef SBRC_MARCH_FASTSEG
 #define SBRC_MARCH_FASTSEG 1  // K2: samples inside the ray's interior t-range skip the cube/face tests
 #endif
@@ -922,6 +925,40 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       // float64 t stays the sample-position authority.
       const float ftx0 = (float)fma(t, txd, tx0), fty0 = (float)fma(t, tyd, ty0), fli0 = (float)fma(t, lid, li0);
       const float ftxs = (float)(txd * step), ftys = (float)(tyd * step), flis = (float)(lid * step);
+      // Samples of the clamp-free (fast) light path form one interval of the
+      // sample counter: (tx, ty, li) are affine in j, so each bound of the
+      // fast test is a half-line in j. Solved once per ray with 0.01 texel /
+      // layer of margin (the per-sample fmaf values deviate by < 1e-4), the
+      // per-sample test is two compares; samples outside take the general
+      // path, which is correct everywhere (SBRC_LIGHT_FASTSEG).
+      float jfast_lo = 1.0f, jfast_hi = 0.0f;
+      // (cone only: the shell's 18 taps gain nothing from it, 4.70 -> 4.76 ms measured)
+      if constexpr (SBRC_LIGHT_FASTSEG && LOOKUP == SBRC_LOOKUP_LINEAR && SHADING == SBRC_SHADE_CONE && CONE_N > 0) {
+        double jl = 0.0, jh = 16777216.0;  // float-exact counter range
+        auto keep = [&](double v0, double vs, double lo, double hi) {  // lo <= v0 + j vs < hi
+          lo += 0.01;
+          hi -= 0.01;
+          if (!(lo < hi)) {  // no fast sample at all (buffer narrower than the kernel's reach)
+            jh = -1.0;
+          } else if (vs == 0.0) {
+            if (!(v0 >= lo && v0 < hi)) jh = -1.0;
+          } else {
+            const double a = (lo - v0) / vs, b = (hi - v0) / vs;
+            jl = fmax(jl, fmin(a, b));
+            jh = fmin(jh, fmax(a, b));
+          }
+        };
+        keep(ftx0, ftxs, reach_x, fast_x_hi - reach_x);
+        keep(fty0, ftys, reach_y, fast_y_hi - reach_y);
+        keep(fli0, flis, (double)CONE_A, (double)fast_l_hi + 1.0);
+        // not degenerate: dperp * t > 1e-12 (with t = t0 + j step, over-estimated for margin)
+        if (dperp > 0.f) jl = fmax(jl, (1e-12 / (double)dperp * 1.01 + 1e-12 - t) / step + 1.0);
+        else jh = -1.0;
+        if (jl <= jh) {
+          jfast_lo = (float)ceil(jl);
+          jfast_hi = (float)floor(jh);
+        }
+      }
       float jf = 0.0f;
       if (G > 1) {  // this lane's first sample: gl steps along the exact float64 chain
         for (int i = 0; i < gl; ++i) t = dadd(t, step);
@@ -1016,9 +1053,11 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
           } else {  // cone
             const bool degenerate = !((double)dperp * t > 1e-12);  // fallback plane_basis(L)[0] = axis_u
             float acc = 0.0f;
-            const bool fast = CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR && !degenerate && tx - reach_x >= 0.f &&
-                              tx + reach_x < fast_x_hi && ty - reach_y >= 0.f && ty + reach_y < fast_y_hi &&
-                              li - (float)CONE_A >= 0.f && li - 1.0f < fast_l_hi;
+            const bool fast = CONE_N > 0 && LOOKUP == SBRC_LOOKUP_LINEAR &&
+                              (SBRC_LIGHT_FASTSEG ? (jf >= jfast_lo && jf <= jfast_hi)
+                                                  : (!degenerate && tx - reach_x >= 0.f && tx + reach_x < fast_x_hi &&
+                                                     ty - reach_y >= 0.f && ty + reach_y < fast_y_hi &&
+                                                     li - (float)CONE_A >= 0.f && li - 1.0f < fast_l_hi));
             if (fast) {
               // every tap inside the buffer: one layer pair per ring, blended once
 #if SBRC_CONE_RING_SERIAL
