@@ -39,25 +39,37 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(verbose: bool = False, force: bool = False, out: str = OUT, defines=(), jobs: int | None = None) -> str:
+def build(verbose: bool = False, force: bool = False, out: str = OUT, defines=(), jobs: int | None = None,
+          unit_defines=None, obj_cache: str | None = None) -> str:
     """Compile every translation unit (in parallel) and link ``out``; ``defines``
-    (e.g. ["SBRC_WIDE_MAX_PIXELS=0"]) and ``out`` build experiment variants."""
+    (e.g. ["SBRC_WIDE_MAX_PIXELS=0"]) and ``out`` build experiment variants.
+    ``unit_defines`` ({"sbrc.cu": [...]}) adds defines to one source only, and
+    ``obj_cache`` (a directory) keeps the objects, reusing each one that is
+    newer than the sources for the same defines — so a K1-only variant
+    recompiles sbrc.cu alone."""
     import concurrent.futures as cf
+    import hashlib
     import tempfile
     srcs = [os.path.join(CSRC, f) for f in SOURCES]
     deps = srcs + [os.path.join(CSRC, "sbrc_common.cuh"), os.path.join(ROOT, "include", "sbrc.h")]
     if not force and os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
         return out
-    tmp = tempfile.mkdtemp(prefix="sbrc_build_")
+    tmp = obj_cache or tempfile.mkdtemp(prefix="sbrc_build_")
+    os.makedirs(tmp, exist_ok=True)
+    newest = max(os.path.getmtime(d) for d in deps)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     extra = [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else [])
 
     def compile_one(unit):
         name, defs = unit
         src = os.path.join(CSRC, name)
-        obj = os.path.join(tmp, "_".join([name] + [d.split("=")[1] for d in defs]) + ".o")
-        res = subprocess.run([nvcc(), *compile_flags, *[f"-D{d}" for d in defs], *extra, "-c", "-o", obj, src],
-                             capture_output=True, text=True)
+        cmd = [nvcc(), *compile_flags, *[f"-D{d}" for d in defs], *extra,
+               *[f"-D{d}" for d in (unit_defines or {}).get(name, ())]]
+        key = hashlib.sha1(" ".join(cmd).encode()).hexdigest()[:12]
+        obj = os.path.join(tmp, "_".join([name] + [d.split("=")[1] for d in defs] + [key]) + ".o")
+        if obj_cache and not verbose and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
+            return src, obj, subprocess.CompletedProcess(cmd, 0, "", "")
+        res = subprocess.run([*cmd, "-c", "-o", obj, src], capture_output=True, text=True)
         return src, obj, res
 
     with cf.ThreadPoolExecutor(max_workers=jobs or min(len(UNITS), os.cpu_count() or 1)) as ex:
