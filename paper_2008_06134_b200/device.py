@@ -451,7 +451,8 @@ def render_params(dvol: DeviceVolume, lut_dev: torch.Tensor, settings, buffer_ca
     keep = [dvol.data, dvol.kernel_data, lut_dev, quads_dev, image, counter]
     if heavy_first:  # dispatch table over the exact grid sbrc_render will launch
         grid = N.render_grid(p)
-        order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, grid, row_range)
+        order = tile_order_for(settings, band_rows, rank, world, lut_dev.device, grid, row_range,
+                               empty_first=image is not None and image.device.type == "cpu")
         if feedback is not None:  # measured order of the previous frame (schedule.TileFeedback)
             order, steps = feedback.prepare(grid, order)
             p.tile_steps = steps.data_ptr()
@@ -466,19 +467,20 @@ _ORDER_CACHE: dict = {}
 
 
 def tile_order_for(settings, band_rows: int, rank: int, world: int, device, grid=None,
-                   row_range=None) -> torch.Tensor:
+                   row_range=None, empty_first: bool = False) -> torch.Tensor:
     """Device copy of the heavy-first dispatch table (schedule.heavy_first) over
     ``grid`` (tiles_x, tiles_y, tile_w, tile_h; default the block grid), cached per view."""
     from .schedule import heavy_first
     cam = settings.camera
     key = (tuple(np.asarray(cam.position, np.float64)), tuple(np.asarray(cam.target, np.float64)),
            tuple(np.asarray(cam.up, np.float64)), float(cam.fov_deg), tuple(settings.viewport), band_rows, rank,
-           world, str(device), None if grid is None else tuple(grid), None if row_range is None else tuple(row_range))
+           world, str(device), None if grid is None else tuple(grid), None if row_range is None else tuple(row_range),
+           bool(empty_first))
     t = _ORDER_CACHE.get(key)
     if t is None:
         # dropping the cache is safe: cached render params own their table (render_params._keep)
         if len(_ORDER_CACHE) > 64:
             _ORDER_CACHE.clear()
-        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world, grid, row_range)).to(device)
+        t = torch.from_numpy(heavy_first(settings, band_rows, rank, world, grid, row_range, empty_first)).to(device)
         _ORDER_CACHE[key] = t
     return t

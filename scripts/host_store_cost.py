@@ -20,7 +20,18 @@ def main():
     dev_img = torch.empty((1024, 1024, 4), device="cuda")
     host_img = torch.empty((1024, 1024, 4), pin_memory=True)
     out = {}
-    for name, img in (("hbm", dev_img), ("host", host_img), ("hbm2", dev_img), ("host2", host_img)):
+    from paper_2008_06134_b200 import device as D, schedule as S
+    hf = S.heavy_first
+
+    def order(empty_first):  # A/B of the host-image tile order (empty tiles first vs last)
+        def patched(settings, band_rows=8, rank=0, world=1, grid=None, row_range=None, ef=False):
+            return hf(settings, band_rows, rank, world, grid, row_range, empty_first and ef)
+        S.heavy_first = patched
+        D._ORDER_CACHE.clear()
+    runs = (("hbm", dev_img, True), ("host_empty_last", host_img, False), ("host", host_img, True),
+            ("hbm2", dev_img, True), ("host_empty_last2", host_img, False), ("host2", host_img, True))
+    for name, img, ef in runs:
+        order(ef)
         for _ in range(3):
             sb.render_device(host_vol, tf, settings, buf, out=img)
         torch.cuda.synchronize()

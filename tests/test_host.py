@@ -225,6 +225,27 @@ def test_tile_feedback_order():
     assert order3.tolist() == [0, 1, 2, 3]                          # new grid: fresh initial order
 
 
+def test_heavy_first_empty_first_order():
+    """schedule.heavy_first: a permutation of the tiles by decreasing estimated
+    cost; with ``empty_first`` (render() into page-locked host memory) the
+    zero-cost tiles lead, in index order, and the rest keep the heavy-first
+    order."""
+    from paper_2008_06134_b200 import scene
+    from paper_2008_06134_b200.schedule import heavy_first, tile_cost
+    s = scene.RenderSettings(camera=scene.Camera(position=(0.5, 0.5, -1.6), target=(0.5, 0.5, 0.5), fov_deg=45.0),
+                             light=scene.Light(direction=(0.3, -0.5, 0.8)), viewport=(96, 80), shading_mode="none")
+    grid = (6, 10, 16, 8)
+    cost = tile_cost(s, grid=grid).reshape(-1)
+    assert (cost == 0).any() and (cost > 0).any()
+    base = heavy_first(s, grid=grid)
+    ef = heavy_first(s, grid=grid, empty_first=True)
+    assert sorted(base.tolist()) == sorted(ef.tolist()) == list(range(60))
+    assert np.all(np.diff(cost[base]) <= 0)
+    n0 = int((cost == 0).sum())
+    assert ef[:n0].tolist() == sorted(np.flatnonzero(cost == 0).tolist())
+    assert ef[n0:].tolist() == [t for t in base.tolist() if cost[t] > 0]
+
+
 @pytest.mark.parametrize("light,res,n", [((0.3, -0.5, 0.8), 48, 24), ((0.0, 0.0, 1.0), 16, 8), ((1.0, 1.0, 1.0), 33, 17)])
 def test_covered_texel_slices_matches_brute_force(light, res, n):
     """bench.covered_texel_slices (the K1 algorithmic-byte count: an analytic
