@@ -515,6 +515,9 @@ __device__ __forceinline__ void tap_rows(const float4* q, size_t off, size_t row
   }
 }
 
+#ifndef SBRC_MARCH_PREFETCH
+#define SBRC_MARCH_PREFETCH 1  // K2 cell prefetch: 1 in the buffer modes, 0 never, 2 always (A/B)
+#endif
 #ifndef SBRC_PREC
 #define SBRC_PREC 0  // experiment: 0 exact float64 sample path; 1 float32 colour; 2 float32 sample
 #endif
@@ -971,9 +974,16 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       // each sample, so the sample that crosses the threshold is kept.
       // the voxel cell of sample j+1 is gathered while sample j is shaded
       // (harmless past the exit: outside the cube nothing is fetched)
+      // PF: sample j+1's cell is gathered into registers while sample j is
+      // shaded. It pays in the buffer modes, whose light lookups have latency
+      // to cover (config 3 cone 2.768 ms vs 3.017 without); `none`, `phong`
+      // and `extinction` gather each cell when it is needed (fewer live
+      // registers: 1.080 -> 0.936, 7.19 -> 6.43, 195 -> 187 ms;
+      // profiles/r2_notes.md). Ray groups always prefetch.
+      constexpr bool PF = G > 1 || SBRC_MARCH_PREFETCH == 2 || (SBRC_MARCH_PREFETCH == 1 && BUFFERED);
       Cell<VT> cur;
-      bool cur_in;
-      {
+      bool cur_in = false;
+      if (PF) {
         const double qx = dadd(P.eye[0], dmul(t, d[0]));
         const double qy = dadd(P.eye[1], dmul(t, d[1]));
         const double qz = dadd(P.eye[2], dmul(t, d[2]));
@@ -1128,21 +1138,29 @@ __global__ void __launch_bounds__(32 * NW, MINB) march_kernel(const sbrc_render_
       };
       if constexpr (G == 1) {
       // One sample: shade the prefetched cell `use` while the next sample's
-      // cell is gathered into `fill`.
-      auto sample = [&](const Cell<VT>& use, const bool use_in, Cell<VT>& fill, bool& fill_in) {
+      // cell is gathered into `fill` (PF), or gather this sample's cell now.
+      auto sample = [&](const Cell<VT>& use_pf, const bool use_in_pf, Cell<VT>& fill, bool& fill_in) {
         const double tn = dadd(t, step);
+        Cell<VT> use_now;
+        bool use_in_now = false;
         {
-          const double qx = dadd(P.eye[0], dmul(tn, d[0]));
-          const double qy = dadd(P.eye[1], dmul(tn, d[1]));
-          const double qz = dadd(P.eye[2], dmul(tn, d[2]));
-          if (UNIT && SBRC_MARCH_FASTSEG && tn >= t_safe_lo && tn <= t_safe_hi) {
-            fill_in = true;
-            cell_fetch_interior<VT>(P.volume, qx, qy, qz, fill);
+          const double tc = PF ? tn : t;  // the cell gathered here: the next sample's (PF) or this one's
+          Cell<VT>& dst = PF ? fill : use_now;
+          bool& dst_in = PF ? fill_in : use_in_now;
+          const double qx = dadd(P.eye[0], dmul(tc, d[0]));
+          const double qy = dadd(P.eye[1], dmul(tc, d[1]));
+          const double qz = dadd(P.eye[2], dmul(tc, d[2]));
+          if (UNIT && SBRC_MARCH_FASTSEG && tc >= t_safe_lo && tc <= t_safe_hi) {
+            dst_in = true;
+            cell_fetch_interior<VT>(P.volume, qx, qy, qz, dst);
           } else {
-            fill_in = in_cube(qx, qy, qz);
-            if (fill_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, fill);
+            dst_in = in_cube(qx, qy, qz);
+            if (dst_in) cell_fetch<VT, UNIT>(P.volume, qx, qy, qz, dst);
           }
         }
+        if (!PF) fill_in = false;
+        const Cell<VT>& use = PF ? use_pf : use_now;
+        const bool use_in = PF ? use_in_pf : use_in_now;
 #if SBRC_PREC == 0
         const double s = use_in ? cell_combine<VT>(use, reinterpret_cast<const float*>(u8tab)) : 0.0;
         const LutPos q = lut_pos(s);
