@@ -779,8 +779,13 @@ def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
     if world > 1:  # page-locked landing buffer for the assembled image (one async D2H per frame)
         host_img = torch.empty((cfg["image"], cfg["image"], 4), dtype=torch.float32).pin_memory()
 
+    from paper_2008_06134_b200.device import drop_frame_constants
+
     def step():
         if world == 1:
+            # every step uploads its own constants (resolved LUTs, slice offsets):
+            # the value cache that would skip unchanged ones is dropped first
+            drop_frame_constants()
             buf = sb.build_attenuation_buffer(host_vol, tf, cam, spec)
             img = sb.render(host_vol, tf, settings, buf)
         else:
@@ -811,7 +816,8 @@ def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
     return {"value": 1.0 / sec, "unit": "frames/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": sec * 1e3, "steps": k, "volume_upload_s_once": upload_s,
             "path": "paper_2008_06134_b200.build_attenuation_buffer + render (numpy in, numpy out; "
-                    "K2 stores the image into pinned host memory)"
+                    "the resolved LUTs and slice offsets uploaded every step; K2 stores the image into "
+                    "pinned host memory)"
             if world == 1 else "FrameRenderer (host LUTs in, host image out)"}
 
 

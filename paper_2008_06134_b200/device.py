@@ -243,6 +243,20 @@ def device_const(arr, device) -> torch.Tensor:
     return t
 
 
+def device_consts(arrs, device) -> list:
+    """Several small float64 host arrays as views of ONE device copy (one
+    pinned staging buffer, one host-to-device copy), cached by value like
+    ``device_const``."""
+    parts = [np.ascontiguousarray(a, dtype=np.float64) for a in arrs]
+    flat = np.concatenate([a.reshape(-1) for a in parts])
+    t = device_const(flat, device)
+    out, o = [], 0
+    for a in parts:
+        out.append(t[o:o + a.size].view(a.shape))
+        o += a.size
+    return out
+
+
 _RESOLVED: dict = {}
 
 
@@ -262,6 +276,17 @@ def resolved_lut(tf, step: float) -> np.ndarray:
             _RESOLVED.clear()
         _RESOLVED[key] = out
     return out
+
+
+def drop_frame_constants() -> None:
+    """Forget the value-cached device copies of the per-frame constants (LUTs,
+    plane offsets), so the next call uploads them again — an end-to-end
+    measurement whose every step pays its own host-to-device copies
+    (bench.py e2e). The memoised LUT resolves (host arithmetic, a pure
+    function of the LUT and step) are kept."""
+    global _CONST_CACHE
+    with _CONST_LOCK:
+        _CONST_CACHE = None
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import (_require_cuda, build_params, current_stream_handle, device_const, device_volume, f64_tensor,
+from .device import (_require_cuda, build_params, current_stream_handle, device_consts, device_volume, f64_tensor,
                      pack_quads, resolved_lut, to_host)
 
 
@@ -184,8 +184,8 @@ def build_attenuation_buffer(v, tf, cam, spec, compensation_n: float = 0.0, devi
     w, h = int(cam.resolution[0]), int(cam.resolution[1])
     n = int(spec.n_slices)
     dvol = device_volume(v, dev)
-    alpha = device_const(resolved_lut(tf, spec.spacing)[:, 3], dev)   # :159-160
-    offsets = device_const(spec.plane_offsets, dev)
+    # alpha LUT at the slice spacing (:159-160) and the plane offsets: one upload
+    alpha, offsets = device_consts((resolved_lut(tf, spec.spacing)[:, 3], spec.plane_offsets), dev)
     quads = torch.empty((n, h, w, 4), dtype=torch.float32, device=dev)
     reach = default_reach(cam, spec, float(dvol.voxel_size.max()))
     build_into(dvol, alpha, cam, spec, offsets, quads, compensation_n, sparse=reach)
