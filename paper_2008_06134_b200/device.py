@@ -30,7 +30,13 @@ def _require_cuda(device=None) -> torch.device:
     return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def current_stream_handle() -> int:
+    """cudaStream_t of the current stream on the current device."""
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 
@@ -205,11 +211,59 @@ def broadcast_volume(dvol: "DeviceVolume | None", dims, voxel_type: int, box_lo,
     return DeviceVolume(t, voxel_type, dims, box_lo, box_hi)
 
 
+class _PinnedRing:
+    """Page-locked staging ring for the small per-frame uploads (LUTs, plane
+    offsets): a host array is copied into the next free slot and sent with one
+    asynchronous copy on the current stream. Slots are handed out in order;
+    the ring wraps only once every copy of the previous lap has completed (at
+    ~12 KiB per frame that is dozens of frames back), so a slot is never
+    rewritten under a copy in flight. While a lap is still in flight (a host
+    far ahead of the GPU) uploads take torch's pinned allocator instead of
+    waiting. ``upload`` returns None then."""
+
+    def __init__(self, nbytes: int = 1 << 20):
+        self.size = nbytes
+        self.off = 0
+        self.buf = None
+        self.host = None
+        self.pending: list = []
+        self.lock = threading.Lock()
+
+    def upload(self, a: np.ndarray, device) -> torch.Tensor | None:
+        nb = a.nbytes
+        with self.lock:
+            if self.buf is None:
+                self.buf = torch.empty(self.size, dtype=torch.uint8, pin_memory=True)
+                self.host = self.buf.numpy()
+            start = (self.off + 255) & ~255
+            if start + nb > self.size:
+                # newest first: on one stream it completes last, so a lap in flight costs one query
+                if not all(ev.query() for ev in reversed(self.pending)):
+                    return None
+                self.pending.clear()
+                start = 0
+            self.host[start:start + nb] = a.reshape(-1).view(np.uint8)
+            dst = torch.empty(a.shape, dtype=torch.float64, device=device)
+            dst.copy_(self.buf[start:start + nb].view(torch.float64).view(a.shape), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(dst.device))
+            self.pending.append(ev)
+            self.off = start + nb
+        return dst
+
+
+_STAGING = _PinnedRing()
+
+
 def f64_tensor(arr, device) -> torch.Tensor:
     """float64 host array -> device, staged through pinned memory and copied
-    asynchronously on the current stream (the pinned block is recycled by
-    torch's caching host allocator once the copy has completed)."""
+    asynchronously on the current stream (small arrays through the staging
+    ring, larger ones through torch's caching host allocator)."""
     a = np.ascontiguousarray(arr, dtype=np.float64)
+    if 0 < a.nbytes <= _STAGING.size // 8 and torch.device(device).type == "cuda":
+        t = _STAGING.upload(a, device)
+        if t is not None:
+            return t
     if not a.flags.writeable:  # read-only cached arrays (scene.camera_frame): torch wants a writable buffer
         a = a.copy()
     host = torch.from_numpy(a)

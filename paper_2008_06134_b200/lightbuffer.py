@@ -145,13 +145,25 @@ def lookup_reach(settings, cam, spec, voxel_size_max: float):
     return (lat + 2.0 * math.sqrt(2.0) * texel, below + 1, above + 1)
 
 
+_REACH: dict = {}
+
+
 def default_reach(cam, spec, voxel_size_max: float):
     """Reach covering the default kernels of every buffer mode (the sparse
-    build of ``build_attenuation_buffer``, whose consumer is not known yet)."""
-    from types import SimpleNamespace
-    reaches = [lookup_reach(SimpleNamespace(shading_mode=m, shell_kernel=None, cone_kernel=None), cam, spec,
-                            voxel_size_max) for m in ("sbrc_shadow", "shell", "cone")]
-    return tuple(max(r[i] for r in reaches) for i in range(3))
+    build of ``build_attenuation_buffer``, whose consumer is not known yet);
+    memoised by the quantities it depends on."""
+    key = (tuple(int(r) for r in cam.resolution), tuple(float(u) for u in cam.u_range),
+           tuple(float(v) for v in cam.v_range), float(spec.spacing), float(voxel_size_max))
+    out = _REACH.get(key)
+    if out is None:
+        from types import SimpleNamespace
+        reaches = [lookup_reach(SimpleNamespace(shading_mode=m, shell_kernel=None, cone_kernel=None), cam, spec,
+                                voxel_size_max) for m in ("sbrc_shadow", "shell", "cone")]
+        out = tuple(max(r[i] for r in reaches) for i in range(3))
+        if len(_REACH) > 256:
+            _REACH.clear()
+        _REACH[key] = out
+    return out
 
 
 def covers(have, need) -> bool:
@@ -160,7 +172,8 @@ def covers(have, need) -> bool:
 
 def check_frame(cam, spec) -> None:
     """lightbuffer.py:155-156: camera and stack must agree on the light direction."""
-    if float(np.linalg.norm(np.asarray(cam.light_dir) - np.asarray(spec.light_dir))) > 1e-9:
+    a, b = cam.light_dir, spec.light_dir  # (3,) each; the norm of the difference, as numpy computes it
+    if len(a) != len(b) or math.sqrt(sum((float(x) - float(y)) ** 2 for x, y in zip(a, b))) > 1e-9:
         raise ValueError("light camera and slice stack disagree on light direction")
 
 

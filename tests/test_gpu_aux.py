@@ -83,3 +83,29 @@ def test_layer_pair_shadow_frames_identical(torch, case):
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
     assert np.array_equal(fr.intensity.cpu().numpy(), g["intensity"])
+
+
+def test_pinned_staging_ring_wraps(torch):
+    """device.f64_tensor's staging ring: uploads across several wrap-arounds
+    (each lap waits for the previous lap's copies) all arrive intact, and
+    device_consts views split one upload correctly."""
+    from paper_2008_06134_b200 import device as D
+    ring = D._PinnedRing(nbytes=64 * 1024)
+    rng = np.random.default_rng(5)
+    sent, fallbacks = [], 0
+    for i in range(300):  # ~ 300 * 2-4 KiB = several laps of 64 KiB
+        a = rng.random(int(rng.integers(1, 512)))
+        t = ring.upload(a, "cuda")
+        if t is None:  # previous lap still in flight: the caller falls back
+            fallbacks += 1
+            torch.cuda.synchronize()
+            t = ring.upload(a, "cuda")
+        sent.append((a, t))
+    torch.cuda.synchronize()
+    for a, t in sent:
+        assert np.array_equal(t.cpu().numpy(), a)
+    D.drop_frame_constants()
+    x, y = rng.random(256), rng.random(37)
+    tx, ty = D.device_consts((x, y), "cuda")
+    assert np.array_equal(tx.cpu().numpy(), x) and np.array_equal(ty.cpu().numpy(), y)
+    assert ty.data_ptr() == tx.data_ptr() + 256 * 8

@@ -119,6 +119,18 @@ def test_validation_mirrors_reference():
     assert issubclass(scene.ConfigError, ValueError)
 
 
+def test_check_frame_light_direction():
+    """lightbuffer.check_frame (lightbuffer.py:155-156): a light camera and a
+    slice stack of different light directions are refused."""
+    from paper_2008_06134_b200 import scene
+    from paper_2008_06134_b200.lightbuffer import check_frame
+    cam = scene.LightCamera.fit((0.3, -0.5, 0.8), (1, 1, 1), (8, 8))
+    check_frame(cam, scene.make_slice_stack((0.3, -0.5, 0.8), 4))
+    check_frame(cam, scene.make_slice_stack((0.6, -1.0, 1.6), 4))  # normalised: the same direction
+    with pytest.raises(ValueError):
+        check_frame(cam, scene.make_slice_stack((0.3, -0.5, 0.81), 4))
+
+
 def test_no_cpu_fallback():
     """Without CUDA the product path raises instead of computing on the CPU."""
     import torch
