@@ -281,3 +281,24 @@ def test_covered_texel_slices_matches_brute_force(light, res, n):
         count += int(np.all((p >= 0.0) & (p <= 1.0), axis=-1).sum())
     got = bench.covered_texel_slices(cam, spec)
     assert abs(got - count) <= 0.005 * count, (got, count)
+
+
+def test_reference_arm_runs_without_the_product_package():
+    """bench.py --impl reference (the driver's reference arm) on config 1: one
+    JSON line from the numpy port on the host cores, exit 0, nothing of the
+    product package (or its CUDA library) imported, the same config keys as
+    the GPU arm, and an e2e entry with no device copies."""
+    import json
+    import subprocess
+    from conftest import ROOT
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "1", "--steps", "1",
+                          "--warmup", "0"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "frames/s"
+    assert d["product_package_loaded"] is False
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
+    assert {"workload", "image", "n_slices", "slice_res", "shading_mode"} <= set(d["config"])
