@@ -789,9 +789,11 @@ def e2e_public(a, cfg, tf, cam, spec, settings, dvol, host_vol, fr, world, dev):
             buf = sb.build_attenuation_buffer(host_vol, tf, cam, spec)
             img = sb.render(host_vol, tf, settings, buf)
         else:
-            fr.lut.copy_(torch.from_numpy(tf.resolve(settings.step)))
-            fr.alpha.copy_(torch.from_numpy(np.ascontiguousarray(tf.resolve(spec.spacing)[:, 3])))
-            fr.offsets.copy_(torch.from_numpy(spec.plane_offsets))
+            # this step's constants, host -> device from page-locked memory
+            for dst, src in ((fr.lut, tf.resolve(settings.step)), (fr.alpha, tf.resolve(spec.spacing)[:, 3]),
+                             (fr.offsets, spec.plane_offsets)):
+                dst.copy_(torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)).pin_memory(),
+                          non_blocking=True)
             host_img.copy_(fr.frame(), non_blocking=True)
             torch.cuda.current_stream().synchronize()
             img = host_img.numpy()
